@@ -1,0 +1,229 @@
+/*
+ * mel.h -- C ABI of the B200-native reservoir-fed surrogate trainer
+ * (arXiv 2309.16743, Meyer et al., "High Throughput Training of Deep Surrogates
+ * from Large Ensemble Runs").  Library: paper_2309_16743_b200/libmel.so.
+ *
+ * Citations are PAPER.md line numbers (P:n) with the section they fall in.
+ *
+ * The calls follow the paper's statement of the problem:
+ *   reservoir_put          <- client `send` of one time step u_X^t (§3.1)
+ *                             into the rank's training buffer (Alg. 1 put)
+ *   reservoir_close        <- "finalize_communication" of the last client /
+ *                             "the reception is over" (Alg. 1)
+ *   reservoir_sample_batch <- the training thread building a batch with b gets
+ *                             (Alg. 1 get, "with replacement")
+ *   surrogate_step         <- forward, MSE, backward, gradient all-reduce, Adam
+ *
+ *   surrogate_eval         <- validation on held-out simulations
+ *
+ * Conventions (all calls):
+ *   - Every call returns an int status (enum mel_status).  Negative = error;
+ *     on error the context state is unchanged, except MEL_ECUDA / MEL_ENCCL which
+ *     poison the context (every later call returns the same code).
+ *     mel_last_error() returns a human-readable message for the last error.
+ *   - Pointers named *_host are host memory owned by the caller, only read or
+ *     written during the call.  Device pointers are accepted only where a
+ *     `*_on_device` flag says so; they are read in stream order on the
+ *     context's stream and must stay valid until the next mel_sync().
+ *   - The context owns all device memory (reservoir slots, staging ring,
+ *     weights, Adam moments, activations, scratch).  Nothing is allocated per
+ *     step.
+ *   - Threads: one thread per context at a time (the caller serialises the
+ *     producer and consumer roles; the order of calls is the op-log, reading R4
+ *     in DESIGN.md).
+ *   - Layout of parameters: tensors in the order W_1, b_1, ..., W_L, b_L, with
+ *     W_l row-major [out][in] fp32, dims = [6, hidden..., n_field].
+ */
+#ifndef MEL_H_
+#define MEL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MEL_ABI_VERSION 1u
+#define MEL_HIST_BINS 64
+#define MEL_MAX_TENSORS 6
+
+enum mel_status {
+  MEL_OK = 0,
+  MEL_EAGAIN = 1,     /* put: staging ring full | sample: p <= theta during reception
+                          | step: no rank has a batch (nothing done)            */
+  MEL_EOS = 2,        /* step: every rank is closed and drained                */
+  MEL_EINVAL = -1,    /* bad argument or configuration                                 */
+  MEL_ECLOSED = -2,   /* put after reservoir_close                                     */
+  MEL_EPROTO = -3,    /* double close                                                  */
+  MEL_ECUDA = -4,     /* CUDA error (context poisoned)                                 */
+  MEL_ENCCL = -5,     /* NCCL error (context poisoned)                                 */
+  MEL_ENOMEM = -6,    /* device allocation failed                                      */
+  MEL_ENONFINITE = -7 /* loss not finite                                               */
+};
+
+enum mel_precision {
+  MEL_FP32 = 0,  /* parity mode: every contraction in fp32 FFMA (SIMT kernels)        */
+  MEL_BF16 = 1   /* bench mode: output layer on tcgen05 (bf16 operands, fp32 TMEM
+                    accumulation), fp32 master weights / Adam / head               */
+};
+
+enum mel_storage {
+  MEL_STORE_F32 = 0,  /* slot stores RN_f32((u - lo) / (hi - lo))                      */
+  MEL_STORE_BF16 = 1  /* slot stores RNE_bf16 of the same fp32 value                    */
+};
+
+typedef struct mel_ctx mel_ctx;
+
+typedef struct {
+  uint32_t abi_version;        /* must be MEL_ABI_VERSION                                */
+  uint32_t n_field;            /* N = n*n outputs ("output of 1M neurons")          */
+  uint32_t hidden[2];          /* hidden widths; {256,256}; tiny {32,0}          */
+  uint32_t capacity;           /* C, reservoir slots per rank (6000)              */
+  uint32_t threshold;          /* theta, watermark (1000); require theta < C      */
+  uint32_t batch;              /* B per rank (10; bench: 1024)                    */
+  uint32_t steps_per_sim;      /* tau, used for the input t/tau (100)             */
+  float temp_lo, temp_hi;      /* normalisation range, 100 / 500 K               */
+  uint32_t precision;          /* enum mel_precision                                     */
+  uint32_t storage;            /* enum mel_storage                                       */
+  double lr0, lr_min;          /* 1e-3, 2.5e-4                            */
+  uint64_t lr_halving_samples; /* 10000 global samples                           */
+  double beta1, beta2, eps;    /* Adam 0.9, 0.999, 1e-8 (reading R15)                    */
+  uint64_t seed;               /* Philox key for SAMPLE/EVICT/DRAIN/INIT streams */
+  uint32_t staging_entries;    /* depth of the pending-put ring (>= 1)                   */
+  uint32_t flags;              /* MEL_FLAG_*                                             */
+} mel_config;
+
+#define MEL_FLAG_TIMING 1u     /* record CUDA events around every kernel (bench roofline) */
+
+typedef struct {
+  uint64_t population, unseen, seen;     /* p, u, s = p - u                            */
+  uint64_t puts;                         /* accepted reservoir_put calls               */
+  uint64_t committed;                    /* q: puts that reached a slot                */
+  uint64_t draws;                        /* d: SAMPLE + DRAIN draws                    */
+  uint64_t evictions;
+  uint64_t pending;                      /* accepted but not committed (back-pressure) */
+  uint64_t steps;                        /* optimiser steps taken (Adam k)             */
+  uint64_t samples;                      /* global samples consumed (LR schedule S)    */
+  uint64_t hist[MEL_HIST_BINS];          /* retired items by final seen count (Fig. 3) */
+  uint32_t over;                         /* reception over and pending empty           */
+  uint32_t closed;
+  double last_loss;                      /* loss of the last completed step            */
+} mel_stats;
+
+/* Fills *cfg with the paper's defaults for the given output width and
+ * batch.  Always succeeds for non-NULL cfg. */
+int mel_config_default(mel_config* cfg, uint32_t n_field, uint32_t batch);
+
+/* Writes a 128-byte NCCL unique id into out128 (host).  Call on rank 0 only, then
+ * broadcast it to every rank (the Python binding uses torch.distributed).
+ * Errors: MEL_ENCCL. */
+int mel_nccl_unique_id(void* out128);
+
+/* Creates a context on `cuda_device`.  world > 1 requires nccl_id (128 B from
+ * mel_nccl_unique_id); world == 1 requires nccl_id == NULL.  cuda_stream: a
+ * cudaStream_t to run on, or NULL for a library-owned stream.  Weights are
+ * initialised from the Philox INIT stream (identical on every rank: reading R13)
+ * unless mel_set_params is called.  Errors: MEL_EINVAL (bad config: n_field == 0,
+ * theta >= C, batch == 0, bf16 mode with the last hidden width not a multiple
+ * of 64, ...), MEL_ECUDA, MEL_ENCCL, MEL_ENOMEM. */
+int mel_create(const mel_config* cfg, int rank, int world, const void* nccl_id,
+               int cuda_device, void* cuda_stream, mel_ctx** out);
+void mel_destroy(mel_ctx* ctx);
+const char* mel_last_error(const mel_ctx* ctx);
+
+/* Number of parameter tensors (2 per layer) and, if shapes != NULL, their
+ * [rows, cols] (cols = 1 for biases).  Total element count in *total. */
+int mel_param_layout(const mel_ctx* ctx, uint32_t* n_tensors, uint32_t* shapes /* 2*n */,
+                     uint64_t* total);
+
+/* Host fp32 parameters in / out (tensor order above).  set: all ranks must set
+ * identical values; resets nothing else.  get synchronises the stream. */
+int mel_set_params(mel_ctx* ctx, const float* const* tensors_host);
+int mel_get_params(mel_ctx* ctx, float* const* tensors_host);
+
+/* Full optimiser state (params, Adam first/second moments, step count k and
+ * global samples S), host fp32.  Used by checkpointing and by the re-anchored
+ * parity harness.  Synchronises. */
+typedef struct {
+  float* const* p;
+  float* const* m;
+  float* const* v;
+  uint64_t adam_step;
+  uint64_t samples_seen;
+} mel_state_view;
+int mel_get_state(mel_ctx* ctx, mel_state_view* out);
+int mel_set_state(mel_ctx* ctx, const mel_state_view* in);
+
+/* Alg. 1 put of one time step (sim_id, t, X[5] kelvin, field[N] fp32
+ * kelvin -- the fp32 wire data of P:210).  The item enters the pending FIFO; it
+ * is committed to a slot at the next commit point (start of
+ * reservoir_sample_batch, or reservoir_close).  field_on_device = 0: field is
+ * host memory, copied before return (pinned memory makes the copy asynchronous);
+ * 1: device pointer, copied in stream order.  Errors: MEL_ECLOSED after close,
+ * MEL_EAGAIN when the staging ring is full (the caller retries after sampling),
+ * MEL_EINVAL. */
+int reservoir_put(mel_ctx* ctx, uint32_t sim_id, uint32_t t, const float X_host[5],
+                  const float* field, int field_on_device);
+
+/* Signals that reception is over ("When all the simulation data have been
+ * generated the blocking related to the threshold is lifted").  Commits pending
+ * puts.  A second call returns MEL_EPROTO. */
+int reservoir_close(mel_ctx* ctx);
+
+/* Alg. 1 get x B, batch-atomic: commit point, watermark gate
+ * (p <= theta -> MEL_EAGAIN during reception), then B Philox draws with
+ * replacement, seen counters updated (unseen -> seen).  After
+ * close the buffer drains: every draw removes its item, the batch may be shorter
+ * than B, and 0 items means this rank is empty.  slots_host (int32[B], nullable)
+ * and n_host (nullable) receive the slot ids / count; either being non-NULL
+ * synchronises the stream, both NULL keeps the call asynchronous (during
+ * reception the count is B). */
+int reservoir_sample_batch(mel_ctx* ctx, int32_t* slots_host, uint32_t* n_host);
+
+/* One training step on the batch of the last reservoir_sample_batch: forward,
+ * MSE loss, backward, mean all-reduce of the gradients over the
+ * `world` ranks (NCCL), Adam with the LR schedule.
+ * COLLECTIVE when world > 1: every rank calls it the same number of times; a rank
+ * without a batch contributes 0 samples.  loss_host (nullable): global mean loss
+ * of this step (synchronises); NULL keeps the step asynchronous.
+ * Returns MEL_OK, MEL_EAGAIN (no rank had samples: nothing done), MEL_EOS (every
+ * rank closed and drained), MEL_ENONFINITE (loss not finite), errors. */
+int surrogate_step(mel_ctx* ctx, double* loss_host);
+
+/* Forward-only validation of n samples given on the host: X_host n x 5
+ * kelvin, t_host n, fields_host n x N fp32 kelvin (nullable: then no MSE).
+ * mse_host (nullable) receives the MSE in normalised units (reading Q13);
+ * pred_host (nullable, n x N) the predictions de-normalised to kelvin.
+ * Synchronises. */
+int surrogate_eval(mel_ctx* ctx, const float* X_host, const uint32_t* t_host,
+                   const float* fields_host, uint32_t n, double* mse_host, float* pred_host);
+
+/* Snapshot of the reservoir and trainer counters (synchronises). */
+int reservoir_stats(mel_ctx* ctx, mel_stats* out);
+
+/* Test/diagnostic view of the reservoir (synchronises).  Each output is nullable
+ * and sized C (payload: C x n_field elements of 4 B for MEL_STORE_F32, 2 B for
+ * MEL_STORE_BF16).  Empty slots report sim = 0xFFFFFFFF. */
+int reservoir_dump(mel_ctx* ctx, uint32_t* sim_host, uint32_t* t_host, float* X_host /*C x 5*/,
+                   uint32_t* seen_host, uint64_t* put_seq_host, void* payload_host);
+
+/* Waits for all work queued on the context's stream. */
+int mel_sync(mel_ctx* ctx);
+
+/* Per-kernel timing (flag MEL_FLAG_TIMING): total milliseconds and launch count
+ * of kernel class `k` (enum mel_kernel) since the last reset, measured with CUDA
+ * events on the launching stream.  Synchronises. */
+enum mel_kernel {
+  MEL_K_COMMIT = 0, MEL_K_SAMPLE, MEL_K_GATHER, MEL_K_HEAD_FWD, MEL_K_OUT_FWD_DW,
+  MEL_K_OUT_DH, MEL_K_HEAD_BWD, MEL_K_ALLREDUCE, MEL_K_ADAM, MEL_K_LOSS, MEL_K_COUNT
+};
+int mel_kernel_time(mel_ctx* ctx, int k, double* ms_host, uint64_t* launches_host);
+int mel_kernel_time_reset(mel_ctx* ctx);
+/* Number of library kernel launches since creation (bench "gpu_launches"). */
+int mel_launch_count(const mel_ctx* ctx, uint64_t* n_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MEL_H_ */

@@ -1,0 +1,63 @@
+// Shared device helpers for libmel (sm_100a).  Product code: nothing here is
+// shared with the CPU oracle (independent numpy), per DESIGN.md "Boundary".
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace mel {
+
+// ---- Philox4x32-10 (Salmon et al., SC'11), stream layout of DESIGN.md ---------
+// key = (lo32(seed), hi32(seed)), counter = (lo32(n), hi32(n), c2, tag)
+enum : uint32_t { TAG_SAMPLE = 1, TAG_EVICT = 2, TAG_DRAIN = 3, TAG_INIT = 4 };
+
+__host__ __device__ __forceinline__ uint32_t mulhi32(uint32_t a, uint32_t b) {
+#ifdef __CUDA_ARCH__
+  return __umulhi(a, b);
+#else
+  return (uint32_t)(((uint64_t)a * b) >> 32);
+#endif
+}
+
+__host__ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    const uint32_t hi0 = mulhi32(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = mulhi32(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+  }
+  return c;
+}
+
+// one 64-bit draw per counter value n: r64 = (o1 << 32) | o0
+__host__ __device__ __forceinline__ uint64_t philox_r64(uint64_t seed, uint32_t tag, uint64_t n, uint32_t c2) {
+  const uint4 o = philox4x32_10(make_uint4((uint32_t)n, (uint32_t)(n >> 32), c2, tag),
+                                (uint32_t)seed, (uint32_t)(seed >> 32));
+  return ((uint64_t)o.y << 32) | o.x;
+}
+
+// floor(r * n / 2^64): no rejection, consumption is one counter per draw
+__host__ __device__ __forceinline__ uint32_t bounded(uint64_t r, uint32_t n) {
+#ifdef __CUDA_ARCH__
+  return (uint32_t)__umul64hi(r, (uint64_t)n);
+#else
+  return (uint32_t)(((unsigned __int128)r * n) >> 64);
+#endif
+}
+
+__host__ __device__ __forceinline__ double unit_double(uint64_t r) {
+  return (double)(r >> 11) * 0x1.0p-53;
+}
+
+// ---- numerics -----------------------------------------------------------------------
+__device__ __forceinline__ float normalise_rn(float u, float lo, float span) {
+  // RN_f32((u - lo) / span), each op correctly rounded (no fast-math contraction)
+  return __fdiv_rn(__fsub_rn(u, lo), span);
+}
+
+__device__ __forceinline__ float bf16_bits_to_f32(uint16_t h) {
+  return __uint_as_float(((uint32_t)h) << 16);
+}
+
+}  // namespace mel

@@ -1,0 +1,115 @@
+// Internal launch interface between the ABI layer (mel.cu) and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace mel {
+
+constexpr int HIST_BINS = 64;
+
+// Reservoir device state (one per rank), DESIGN.md "Data layout in HBM".
+struct ResDev {
+  uint64_t q;          // committed puts (put_seq of the next item)
+  uint64_t d;          // draws (SAMPLE + DRAIN counters)
+  uint64_t evictions;
+  uint64_t consumed;   // staging-ring entries consumed by commits
+  uint32_t p;          // population
+  uint32_t u;          // unseen items
+  uint32_t over;       // closed && pending empty
+  uint32_t n_last;     // size of the last batch (0 = EAGAIN / empty)
+  uint32_t n_plan;     // entries committed by the last commit
+  uint32_t pad;
+  uint64_t hist[HIST_BINS];
+};
+
+// Host-visible mirror (mapped pinned memory), written at the end of the
+// reservoir kernels and of the step; read by the host after a stream sync.
+struct Mirror {
+  uint64_t consumed, q, d, evictions;
+  uint32_t p, u, over, n_last;
+  uint64_t adam_k, samples;
+  double loss;
+  double n_total;
+  int32_t status;      // step: 0 ok, 1 skip (no samples)
+  uint32_t pad;
+};
+
+struct StMeta {        // staging-ring metadata (32 B)
+  uint32_t sim, t;
+  float X[5];
+  uint32_t pad;
+};
+typedef StMeta SlotMeta;
+
+// per-step scalars computed on device (loss finalize -> Adam)
+struct StepDev {
+  double red[2];       // [sse, n] (all-reduced when world > 1)
+  double loss;
+  float scale;         // 1 / (N * n_total)
+  float lr, c1, c2;    // lr and Adam bias corrections 1 - beta^k
+  uint64_t k, S;       // Adam step, global samples consumed
+  int32_t skip;        // no samples this step
+  int32_t nonfinite;
+};
+
+struct ResArgs {
+  ResDev* st;
+  Mirror* mirror;
+  const StMeta* st_meta;
+  const float* st_field;     // staging ring [S][Npad] fp32 kelvin
+  uint32_t S;
+  SlotMeta* meta;            // [C]
+  uint32_t* seen;            // [C]
+  uint64_t* put_seq;         // [C]
+  uint32_t* bitmap;          // [ceil(C/32)]
+  uint32_t* pos;             // [C]
+  void* payload;             // [C][Npad] f32 or bf16
+  uint32_t C, theta;
+  uint64_t Npad;
+  uint32_t N;
+  int storage;
+  float lo, span;
+  uint64_t seed;
+  uint32_t rank;
+  uint2* plan;               // [S] (entry, slot)
+};
+
+// reservoir.cu
+void launch_commit(const ResArgs& a, uint64_t tail, uint32_t closed, uint32_t max_entries, cudaStream_t s);
+void launch_sample(const ResArgs& a, int32_t* slots, uint32_t B, cudaStream_t s);
+void launch_gather(const ResArgs& a, const int32_t* slots, uint32_t B, uint32_t tau, float* xn, cudaStream_t s);
+void launch_init_res(const ResArgs& a, cudaStream_t s);
+
+// mlp_simt.cu
+enum Epi { EPI_STORE = 0, EPI_BIAS_RELU = 1, EPI_BIAS = 2 };
+void sgemm(bool ta, bool tb, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
+           float* C, int ldc, int epi, const float* bias, float* H, int ldh, int splits, cudaStream_t s);
+void splitk_reduce(int M, int N, int splits, const float* part, float* C, int ldc, const float* relu_mask,
+                   int ldm, cudaStream_t s);
+struct OutArgs {
+  const float* H; int ldh;        // [B][K]
+  const float* W; const float* b; // W [Npad][K], b [Npad]
+  int K;
+  const void* payload; int storage; uint64_t Npad; uint32_t N;
+  const int32_t* slots; const ResDev* st;   // n_valid = st->n_last
+  float* dY;                      // [B][Npad] raw dS/dY = 2 (Y - T) (0 outside valid)
+  double* sse_part;               // per-block partial sums
+  int B;
+};
+int out_fwd_f32(const OutArgs& a, cudaStream_t s);   // returns number of partials
+void col_sum(const float* X, int rows, int cols, int ld, float* out, cudaStream_t s);
+void reduce_local(StepDev* sd, const double* parts, int n_parts, const ResDev* st, cudaStream_t s);
+void step_finalize(StepDev* sd, double n_field, double lr0, double lr_min, uint64_t halving, double b1, double b2,
+                   Mirror* mirror, ResDev* st, cudaStream_t s);
+void adam_flat(float* p, float* m, float* v, const float* g, uint64_t n, const StepDev* sd,
+               float b1, float b2, float eps, __nv_bfloat16* shadow, uint64_t sh_begin, uint64_t sh_end,
+               cudaStream_t s);
+void init_tensor(float* dst, uint64_t count, uint32_t tid, uint32_t fan_in, uint64_t seed, cudaStream_t s);
+void to_bf16(const float* src, __nv_bfloat16* dst, uint64_t n, cudaStream_t s);
+void relu_mask_mul(float* X, const float* Z, uint64_t n, cudaStream_t s);
+int eval_mse_partial(const float* Y, const float* T, int rows, int cols, int ld, double* part, cudaStream_t s);
+void eval_inputs(const float* X, const uint32_t* t, int n, uint32_t tau, float lo, float span, float* xn, cudaStream_t s);
+void normalise_fields(const float* src, float* dst, uint64_t n, float lo, float span, cudaStream_t s);
+
+}  // namespace mel

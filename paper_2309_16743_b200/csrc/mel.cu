@@ -1,0 +1,899 @@
+// libmel C ABI (include/mel.h): context, device arenas, streams, op sequencing
+// of the reservoir-fed training step, NCCL gradient all-reduce.  Host logic only;
+// every step of the method runs in the kernels of reservoir.cu, mlp_simt.cu and
+// tc_out.cu.
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mel.h"
+#include "kernels.h"
+#include "tc_out.h"
+
+using namespace mel;
+
+namespace {
+
+struct TimedPair {
+  int k;
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct mel_ctx {
+  mel_config cfg{};
+  int rank = 0, world = 1, dev = 0;
+  cudaStream_t stream = nullptr, copy_stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int poisoned = 0;
+
+  // model geometry
+  int L = 0;                       // number of weight layers
+  uint32_t dims[4] = {0, 0, 0, 0}; // [6, hidden..., N]
+  uint32_t N = 0, B = 0, C = 0, Klast = 0, hmax = 0;
+  uint64_t Npad = 0;
+  uint64_t off[2 * 3] = {};        // tensor offsets in the flat buffers
+  uint64_t cnt[2 * 3] = {};
+  uint64_t n_flat = 0;
+
+  // reservoir
+  ResArgs ra{};
+  ResDev* d_st = nullptr;
+  Mirror* h_mirror = nullptr;
+  Mirror* d_mirror = nullptr;
+  StMeta* h_stmeta = nullptr;      // pinned ring mirror of staging metadata
+  uint64_t tail = 0;               // accepted puts
+  uint64_t known_consumed = 0;
+  bool closed = false;
+  bool copy_pending = false;
+  cudaEvent_t ev_copy = nullptr;
+  int32_t* d_slots = nullptr;
+  bool batch_known = false;        // host knows the last batch size
+  uint32_t batch_n = 0;
+
+  // parameters (flat fp32: p, m, v, g) and the bf16 shadow(s) of the output layer
+  float *d_p = nullptr, *d_m = nullptr, *d_v = nullptr, *d_g = nullptr;
+  __nv_bfloat16* d_shadow[2] = {nullptr, nullptr};
+  int shadow_cur = 0;
+
+  // activations / scratch
+  float* d_xn = nullptr;           // [B][8]
+  float* d_z[2] = {nullptr, nullptr};
+  float* d_h[2] = {nullptr, nullptr};
+  float* d_dz[2] = {nullptr, nullptr};
+  float* d_dy = nullptr;           // fp32 mode [B][Npad]
+  float* d_part = nullptr;         // split-K partials
+  size_t part_elems = 0;
+  double* d_sse_part = nullptr;
+  int max_parts = 0;
+  StepDev* d_sd = nullptr;
+  tc::TcBuffers tcb{};
+
+  // eval scratch (lazy)
+  float* d_eval_x = nullptr; uint32_t* d_eval_t = nullptr; float* d_eval_y = nullptr; float* d_eval_f = nullptr;
+  float *d_eval_z[2] = {nullptr, nullptr}, *d_eval_h[2] = {nullptr, nullptr}; float* d_eval_xn = nullptr;
+
+  ncclComm_t comm = nullptr;
+
+  // timing
+  std::vector<TimedPair> pending;
+  std::vector<cudaEvent_t> ev_pool;
+  double kms[MEL_K_COUNT] = {};
+  uint64_t klaunch[MEL_K_COUNT] = {};
+  uint64_t launches = 0;
+};
+
+namespace {
+
+int fail(mel_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) {
+    c->err = buf;
+    if (code == MEL_ECUDA || code == MEL_ENCCL) c->poisoned = code;
+  }
+  return code;
+}
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(c, MEL_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                 \
+  } while (0)
+
+#define NK(call)                                                                                \
+  do {                                                                                          \
+    ncclResult_t r_ = (call);                                                                   \
+    if (r_ != ncclSuccess) return fail(c, MEL_ENCCL, "%s failed: %s", #call, ncclGetErrorString(r_)); \
+  } while (0)
+
+#define GUARD(c)                                 \
+  do {                                           \
+    if (!(c)) return MEL_EINVAL;                 \
+    if ((c)->poisoned) return (c)->poisoned;     \
+    cudaSetDevice((c)->dev);                     \
+  } while (0)
+
+template <class T>
+int dalloc(mel_ctx* c, T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, MEL_ENOMEM, "cudaMalloc(%zu bytes) failed: %s", count * sizeof(T), cudaGetErrorString(e));
+  }
+  return MEL_OK;
+}
+
+#define DALLOC(p, n)                      \
+  do {                                    \
+    int r_ = dalloc(c, &(p), (size_t)(n)); \
+    if (r_) return r_;                    \
+  } while (0)
+
+cudaEvent_t take_event(mel_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// RAII-free timing brackets around one launch group of kernel class k
+struct Timer {
+  mel_ctx* c; int k; cudaEvent_t a = nullptr;
+  Timer(mel_ctx* c_, int k_, int nlaunch) : c(c_), k(k_) {
+    c->launches += nlaunch;
+    c->klaunch[k] += nlaunch;
+    if (c->cfg.flags & MEL_FLAG_TIMING) { a = take_event(c); cudaEventRecord(a, c->stream); }
+  }
+  ~Timer() {
+    if (a) {
+      cudaEvent_t b = take_event(c);
+      cudaEventRecord(b, c->stream);
+      c->pending.push_back({k, a, b});
+    }
+  }
+};
+
+void drain_timers(mel_ctx* c) {
+  for (auto& t : c->pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(t.b);
+    cudaEventElapsedTime(&ms, t.a, t.b);
+    c->kms[t.k] += ms;
+    c->ev_pool.push_back(t.a);
+    c->ev_pool.push_back(t.b);
+  }
+  c->pending.clear();
+}
+
+int check_launch(mel_ctx* c, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(c, MEL_ECUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
+  return MEL_OK;
+}
+
+int sync_stream(mel_ctx* c) {
+  CK(cudaStreamSynchronize(c->stream));
+  c->known_consumed = c->h_mirror->consumed;
+  return MEL_OK;
+}
+
+int validate(const mel_config* g, int world, mel_ctx* c) {
+  if (g->abi_version != MEL_ABI_VERSION) return fail(c, MEL_EINVAL, "abi_version %u != %u", g->abi_version, MEL_ABI_VERSION);
+  if (g->n_field == 0) return fail(c, MEL_EINVAL, "n_field must be > 0");
+  if (g->hidden[0] == 0) return fail(c, MEL_EINVAL, "hidden[0] must be > 0");
+  if (g->capacity == 0 || g->threshold >= g->capacity) return fail(c, MEL_EINVAL, "require threshold < capacity (P:321)");
+  if (g->batch == 0) return fail(c, MEL_EINVAL, "batch must be > 0");
+  if (g->steps_per_sim == 0) return fail(c, MEL_EINVAL, "steps_per_sim must be > 0");
+  if (!(g->temp_hi > g->temp_lo)) return fail(c, MEL_EINVAL, "temp_hi must exceed temp_lo");
+  if (g->precision > MEL_BF16 || g->storage > MEL_STORE_BF16) return fail(c, MEL_EINVAL, "bad precision/storage");
+  if (g->staging_entries == 0) return fail(c, MEL_EINVAL, "staging_entries must be >= 1");
+  if (g->lr_halving_samples == 0) return fail(c, MEL_EINVAL, "lr_halving_samples must be > 0");
+  const uint32_t klast = g->hidden[1] ? g->hidden[1] : g->hidden[0];
+  if (g->precision == MEL_BF16) {
+    if (klast % 64 != 0 || klast > 256) return fail(c, MEL_EINVAL, "bf16 mode needs the last hidden width in {64,128,192,256}");
+    if (g->batch % 64 != 0) return fail(c, MEL_EINVAL, "bf16 mode needs batch %% 64 == 0");
+    if (g->storage != MEL_STORE_BF16) return fail(c, MEL_EINVAL, "bf16 mode stores targets as bf16 (MEL_STORE_BF16)");
+  }
+  if (world < 1) return fail(c, MEL_EINVAL, "world must be >= 1");
+  return MEL_OK;
+}
+
+int ensure_ring_space(mel_ctx* c) {
+  const uint32_t S = c->cfg.staging_entries;
+  if (c->tail - c->known_consumed < S) return MEL_OK;
+  int r = sync_stream(c);
+  if (r) return r;
+  if (c->tail - c->known_consumed < S) return MEL_OK;
+  return MEL_EAGAIN;
+}
+
+int commit(mel_ctx* c) {
+  const uint64_t max_e = c->tail - c->known_consumed;
+  if (c->copy_pending) {
+    CK(cudaStreamWaitEvent(c->stream, c->ev_copy, 0));
+    c->copy_pending = false;
+  }
+  {
+    Timer t(c, MEL_K_COMMIT, max_e ? 2 : 1);
+    launch_commit(c->ra, c->tail, c->closed ? 1u : 0u, (uint32_t)max_e, c->stream);
+  }
+  return check_launch(c, "commit");
+}
+
+int world_allreduce(mel_ctx* c) {
+  if (c->world == 1) return MEL_OK;
+  Timer t(c, MEL_K_ALLREDUCE, 0);
+  NK(ncclGroupStart());
+  NK(ncclAllReduce(c->d_g, c->d_g, c->n_flat, ncclFloat32, ncclSum, c->comm, c->stream));
+  NK(ncclAllReduce(c->d_sd->red, c->d_sd->red, 2, ncclFloat64, ncclSum, c->comm, c->stream));
+  NK(ncclGroupEnd());
+  return MEL_OK;
+}
+
+// backward of the head layers given dZ of the last hidden layer (d_dz[L-2])
+int head_backward(mel_ctx* c) {
+  const int L = c->L;
+  Timer t(c, MEL_K_HEAD_BWD, 3 * (L - 1));
+  for (int l = L - 1; l >= 1; --l) {             // weight layer l (1-based), l < L
+    const int dout = c->dims[l], din = c->dims[l - 1];
+    const float* dZ = c->d_dz[l - 1];
+    const float* Hin = (l == 1) ? c->d_xn : c->d_h[l - 2];
+    const int ldin = (l == 1) ? 8 : din;
+    float* gW = c->d_g + c->off[2 * (l - 1)];
+    float* gb = c->d_g + c->off[2 * (l - 1) + 1];
+    sgemm(true, false, dout, din, (int)c->B, dZ, dout, Hin, ldin, gW, din, EPI_STORE, nullptr, nullptr, 0, 1, c->stream);
+    col_sum(dZ, (int)c->B, dout, dout, gb, c->stream);
+    if (l > 1) {
+      const float* W = c->d_p + c->off[2 * (l - 1)];
+      sgemm(false, false, (int)c->B, din, dout, dZ, dout, W, din, c->d_dz[l - 2], din, EPI_STORE, nullptr, nullptr, 0, 1,
+            c->stream);
+      relu_mask_mul(c->d_dz[l - 2], c->d_z[l - 2], (uint64_t)c->B * din, c->stream);
+    }
+  }
+  return check_launch(c, "head backward");
+}
+
+int head_forward(mel_ctx* c, const float* xn, float** Z, float** H, int rows) {
+  for (int l = 1; l < c->L; ++l) {
+    const int din = c->dims[l - 1], dout = c->dims[l];
+    const float* Hin = (l == 1) ? xn : H[l - 2];
+    const int ldin = (l == 1) ? 8 : din;
+    sgemm(false, true, rows, dout, din, Hin, ldin, c->d_p + c->off[2 * (l - 1)], din, Z[l - 1], dout, EPI_BIAS_RELU,
+          c->d_p + c->off[2 * (l - 1) + 1], H[l - 1], dout, 1, c->stream);
+  }
+  return MEL_OK;
+}
+
+int splits_for(uint64_t K) {
+  int s = (int)(K / 8192);
+  if (s < 1) s = 1;
+  if (s > 64) s = 64;
+  return s;
+}
+
+int train_step_fp32(mel_ctx* c) {
+  const int L = c->L;
+  const uint32_t B = c->B, K = c->Klast;
+  float* Hl = c->d_h[L - 2];
+  const float* WL = c->d_p + c->off[2 * (L - 1)];
+  const float* bL = c->d_p + c->off[2 * (L - 1) + 1];
+  int nparts;
+  {
+    Timer t(c, MEL_K_OUT_FWD_DW, 3);
+    OutArgs oa{Hl, (int)K, WL, bL, (int)K, c->ra.payload, c->ra.storage, c->Npad, c->N, c->d_slots, c->d_st,
+               c->d_dy, c->d_sse_part, (int)B};
+    nparts = out_fwd_f32(oa, c->stream);
+    // dW_L = dY^T H  (M = Npad, N = K, K = B)
+    sgemm(true, false, (int)c->Npad, (int)K, (int)B, c->d_dy, (int)c->Npad, Hl, (int)K, c->d_g + c->off[2 * (L - 1)],
+          (int)K, EPI_STORE, nullptr, nullptr, 0, 1, c->stream);
+    col_sum(c->d_dy, (int)B, (int)c->Npad, (int)c->Npad, c->d_g + c->off[2 * (L - 1) + 1], c->stream);
+  }
+  {
+    Timer t(c, MEL_K_OUT_DH, 2);
+    // dH = dY W  (M = B, N = K, K = Npad), split-K, then ReLU' mask -> dZ_{L-1}
+    const int sp = splits_for(c->Npad);
+    sgemm(false, false, (int)B, (int)K, (int)c->Npad, c->d_dy, (int)c->Npad, WL, (int)K, c->d_part, (int)K, EPI_STORE,
+          nullptr, nullptr, 0, sp, c->stream);
+    splitk_reduce((int)B, (int)K, sp, c->d_part, c->d_dz[L - 2], (int)K, c->d_z[L - 2], (int)K, c->stream);
+  }
+  int r = check_launch(c, "output layer fp32");
+  if (r) return r;
+  reduce_local(c->d_sd, c->d_sse_part, nparts, c->d_st, c->stream);
+  return MEL_OK;
+}
+
+int train_step_bf16(mel_ctx* c) {
+  const int L = c->L;
+  const uint32_t B = c->B, K = c->Klast;
+  {
+    Timer t(c, MEL_K_HEAD_FWD, 1);
+    to_bf16(c->d_h[L - 2], c->tcb.h_bf16, (uint64_t)B * K, c->stream);
+  }
+  tc::OutTcArgs a{};
+  a.N = c->N; a.Npad = c->Npad; a.B = B; a.K = K;
+  a.w_bf16 = c->d_shadow[c->shadow_cur];
+  a.b = c->d_p + c->off[2 * (L - 1) + 1];
+  a.h_bf16 = c->tcb.h_bf16;
+  a.payload = static_cast<const __nv_bfloat16*>(c->ra.payload);
+  a.slots = c->d_slots; a.st = c->d_st;
+  a.dyT = c->tcb.dyT;
+  a.gW = c->d_g + c->off[2 * (L - 1)];
+  a.gb = c->d_g + c->off[2 * (L - 1) + 1];
+  a.sse_part = c->d_sse_part;
+  a.dh_part = c->d_part;
+  a.dz = c->d_dz[L - 2];
+  a.z = c->d_z[L - 2];
+  int nparts = 0;
+  {
+    Timer t(c, MEL_K_OUT_FWD_DW, 1);
+    nparts = tc::launch_out_fwd_dw(a, c->tcb, c->stream);
+  }
+  {
+    Timer t(c, MEL_K_OUT_DH, 2);
+    tc::launch_out_dh(a, c->tcb, c->stream);
+  }
+  int r = check_launch(c, "output layer tcgen05");
+  if (r) return r;
+  reduce_local(c->d_sd, c->d_sse_part, nparts, c->d_st, c->stream);
+  return MEL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mel_config_default(mel_config* g, uint32_t n_field, uint32_t batch) {
+  if (!g) return MEL_EINVAL;
+  memset(g, 0, sizeof *g);
+  g->abi_version = MEL_ABI_VERSION;
+  g->n_field = n_field;
+  g->hidden[0] = 256; g->hidden[1] = 256;
+  g->capacity = 6000; g->threshold = 1000;
+  g->batch = batch;
+  g->steps_per_sim = 100;
+  g->temp_lo = 100.f; g->temp_hi = 500.f;
+  g->precision = MEL_FP32; g->storage = MEL_STORE_F32;
+  g->lr0 = 1e-3; g->lr_min = 2.5e-4; g->lr_halving_samples = 10000;
+  g->beta1 = 0.9; g->beta2 = 0.999; g->eps = 1e-8;
+  g->seed = 1;
+  g->staging_entries = 16;
+  return MEL_OK;
+}
+
+int mel_nccl_unique_id(void* out128) {
+  if (!out128) return MEL_EINVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return MEL_ENCCL;
+  memcpy(out128, &id, sizeof id);
+  return MEL_OK;
+}
+
+const char* mel_last_error(const mel_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, void* stream) {
+  int r = validate(g, c->world, c);
+  if (r) return r;
+  if ((c->world > 1) != (nccl_id != nullptr)) return fail(c, MEL_EINVAL, "nccl_id must be given iff world > 1");
+  c->cfg = *g;
+  CK(cudaSetDevice(c->dev));
+  if (stream) { c->stream = (cudaStream_t)stream; }
+  else { CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)); c->own_stream = true; }
+  CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming));
+
+  // geometry: dims = [6, hidden..., N]
+  c->dims[0] = 6;
+  int nd = 1;
+  c->dims[nd++] = g->hidden[0];
+  if (g->hidden[1]) c->dims[nd++] = g->hidden[1];
+  c->dims[nd++] = g->n_field;
+  c->L = nd - 1;
+  c->N = g->n_field; c->B = g->batch; c->C = g->capacity;
+  c->Npad = ((uint64_t)c->N + 127) / 128 * 128;
+  c->Klast = c->dims[c->L - 1];
+  c->hmax = g->hidden[0] > g->hidden[1] ? g->hidden[0] : g->hidden[1];
+  uint64_t o = 0;
+  for (int l = 0; l < c->L; ++l) {
+    const uint64_t rows = (l == c->L - 1) ? c->Npad : c->dims[l + 1];
+    c->off[2 * l] = o; c->cnt[2 * l] = rows * c->dims[l];
+    o += (c->cnt[2 * l] + 15) / 16 * 16;
+    c->off[2 * l + 1] = o; c->cnt[2 * l + 1] = rows;
+    o += (rows + 15) / 16 * 16;
+  }
+  c->n_flat = o;
+
+  // reservoir arenas
+  const uint32_t S = g->staging_entries, C = g->capacity;
+  ResArgs& a = c->ra;
+  DALLOC(c->d_st, 1);
+  CK(cudaMemset(c->d_st, 0, sizeof(ResDev)));
+  CK(cudaHostAlloc((void**)&c->h_mirror, sizeof(Mirror), cudaHostAllocMapped));
+  memset(c->h_mirror, 0, sizeof(Mirror));
+  CK(cudaHostGetDevicePointer((void**)&c->d_mirror, c->h_mirror, 0));
+  CK(cudaHostAlloc((void**)&c->h_stmeta, sizeof(StMeta) * S, cudaHostAllocDefault));
+  StMeta* d_stmeta; float* d_stfield;
+  DALLOC(d_stmeta, S);
+  DALLOC(d_stfield, (size_t)S * c->Npad);
+  CK(cudaMemset(d_stfield, 0, sizeof(float) * (size_t)S * c->Npad));
+  DALLOC(a.meta, C);
+  DALLOC(a.seen, C);
+  DALLOC(a.put_seq, C);
+  DALLOC(a.bitmap, (C + 31) / 32);
+  CK(cudaMemset(a.bitmap, 0, sizeof(uint32_t) * ((C + 31) / 32)));
+  DALLOC(a.pos, C);
+  const size_t esz = g->storage == MEL_STORE_F32 ? 4 : 2;
+  {
+    void* pl = nullptr;
+    cudaError_t e = cudaMalloc(&pl, esz * (size_t)C * c->Npad);
+    if (e != cudaSuccess) { cudaGetLastError(); return fail(c, MEL_ENOMEM, "reservoir payload (%zu B): %s", esz * (size_t)C * c->Npad, cudaGetErrorString(e)); }
+    CK(cudaMemset(pl, 0, esz * (size_t)C * c->Npad));
+    a.payload = pl;
+  }
+  DALLOC(a.plan, S);
+  a.st = c->d_st; a.mirror = c->d_mirror; a.st_meta = d_stmeta; a.st_field = d_stfield; a.S = S;
+  a.C = C; a.theta = g->threshold; a.Npad = c->Npad; a.N = c->N; a.storage = (int)g->storage;
+  a.lo = g->temp_lo; a.span = g->temp_hi - g->temp_lo; a.seed = g->seed; a.rank = (uint32_t)c->rank;
+  launch_init_res(a, c->stream);
+  DALLOC(c->d_slots, c->B);
+
+  // parameters
+  DALLOC(c->d_p, c->n_flat); DALLOC(c->d_m, c->n_flat); DALLOC(c->d_v, c->n_flat); DALLOC(c->d_g, c->n_flat);
+  CK(cudaMemset(c->d_p, 0, 4 * c->n_flat)); CK(cudaMemset(c->d_m, 0, 4 * c->n_flat));
+  CK(cudaMemset(c->d_v, 0, 4 * c->n_flat)); CK(cudaMemset(c->d_g, 0, 4 * c->n_flat));
+  for (int l = 0; l < c->L; ++l) {
+    const uint64_t rows = c->dims[l + 1];     // real rows (padding rows stay zero)
+    init_tensor(c->d_p + c->off[2 * l], rows * c->dims[l], 2 * l, c->dims[l], g->seed, c->stream);
+    init_tensor(c->d_p + c->off[2 * l + 1], rows, 2 * l + 1, c->dims[l], g->seed, c->stream);
+  }
+  // activations
+  DALLOC(c->d_xn, (size_t)c->B * 8);
+  CK(cudaMemset(c->d_xn, 0, sizeof(float) * c->B * 8));
+  for (int l = 0; l < c->L - 1; ++l) {
+    DALLOC(c->d_z[l], (size_t)c->B * c->dims[l + 1]);
+    DALLOC(c->d_h[l], (size_t)c->B * c->dims[l + 1]);
+    DALLOC(c->d_dz[l], (size_t)c->B * c->dims[l + 1]);
+  }
+  DALLOC(c->d_sd, 1);
+  CK(cudaMemset(c->d_sd, 0, sizeof(StepDev)));
+  if (g->precision == MEL_FP32) {
+    DALLOC(c->d_dy, (size_t)c->B * c->Npad);
+    const int sp = splits_for(c->Npad);
+    c->part_elems = (size_t)sp * c->B * c->Klast;
+    DALLOC(c->d_part, c->part_elems);
+    c->max_parts = (int)(((c->Npad + 63) / 64) * ((c->B + 63) / 64));
+    DALLOC(c->d_sse_part, c->max_parts);
+  } else {
+    DALLOC(c->d_shadow[0], (size_t)c->Npad * c->Klast);
+    r = tc::alloc_buffers(c->tcb, c->Npad, c->B, c->Klast);
+    if (r) return fail(c, MEL_ENOMEM, "tensor-core scratch allocation failed");
+    c->part_elems = tc::dh_part_elems(c->B, c->Klast);
+    DALLOC(c->d_part, c->part_elems);
+    c->max_parts = tc::max_sse_parts(c->Npad);
+    DALLOC(c->d_sse_part, c->max_parts);
+    to_bf16(c->d_p + c->off[2 * (c->L - 1)], c->d_shadow[0], c->Npad * c->Klast, c->stream);
+    r = tc::prepare(c->tcb, c->Npad, c->B, c->Klast, c->d_shadow[0]);
+    if (r) return fail(c, MEL_ECUDA, "tensor-core kernel setup failed: %s", tc::last_error());
+  }
+  r = check_launch(c, "create");
+  if (r) return r;
+  CK(cudaStreamSynchronize(c->stream));
+
+  if (c->world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, sizeof id);
+    NK(ncclCommInitRank(&c->comm, c->world, id, c->rank));
+  }
+  return MEL_OK;
+}
+
+int mel_create(const mel_config* g, int rank, int world, const void* nccl_id, int cuda_device, void* stream,
+               mel_ctx** out) {
+  if (!g || !out) return MEL_EINVAL;
+  *out = nullptr;
+  mel_ctx* c = new mel_ctx();
+  c->rank = rank; c->world = world; c->dev = cuda_device;
+  int r = create_impl(c, g, nccl_id, stream);
+  if (r) {
+    static thread_local std::string last;
+    last = c->err;
+    fprintf(stderr, "mel_create: %s\n", c->err.c_str());
+    mel_destroy(c);
+    return r;
+  }
+  *out = c;
+  return MEL_OK;
+}
+
+void mel_destroy(mel_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->dev);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm) ncclCommDestroy(c->comm);
+  drain_timers(c);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  void* ptrs[] = {c->d_st, (void*)c->ra.st_meta, (void*)c->ra.st_field, c->ra.meta, c->ra.seen, c->ra.put_seq,
+                  c->ra.bitmap, c->ra.pos, c->ra.payload, c->ra.plan, c->d_slots, c->d_p, c->d_m, c->d_v, c->d_g,
+                  c->d_shadow[0], c->d_shadow[1], c->d_xn, c->d_z[0], c->d_z[1], c->d_h[0], c->d_h[1], c->d_dz[0],
+                  c->d_dz[1], c->d_dy, c->d_part, c->d_sse_part, c->d_sd, c->d_eval_x, c->d_eval_t, c->d_eval_y,
+                  c->d_eval_f, c->d_eval_z[0], c->d_eval_z[1], c->d_eval_h[0], c->d_eval_h[1], c->d_eval_xn};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  tc::free_buffers(c->tcb);
+  if (c->h_mirror) cudaFreeHost(c->h_mirror);
+  if (c->h_stmeta) cudaFreeHost(c->h_stmeta);
+  if (c->ev_copy) cudaEventDestroy(c->ev_copy);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int mel_param_layout(const mel_ctx* c, uint32_t* n_tensors, uint32_t* shapes, uint64_t* total) {
+  if (!c) return MEL_EINVAL;
+  if (n_tensors) *n_tensors = 2 * c->L;
+  uint64_t t = 0;
+  for (int l = 0; l < c->L; ++l) {
+    if (shapes) {
+      shapes[4 * l + 0] = c->dims[l + 1]; shapes[4 * l + 1] = c->dims[l];
+      shapes[4 * l + 2] = c->dims[l + 1]; shapes[4 * l + 3] = 1;
+    }
+    t += (uint64_t)c->dims[l + 1] * c->dims[l] + c->dims[l + 1];
+  }
+  if (total) *total = t;
+  return MEL_OK;
+}
+
+static int copy_tensors(mel_ctx* c, float* base, float* const* host, bool to_host) {
+  for (int l = 0; l < c->L; ++l) {
+    for (int w = 0; w < 2; ++w) {
+      const uint64_t n = w == 0 ? (uint64_t)c->dims[l + 1] * c->dims[l] : c->dims[l + 1];
+      float* d = base + c->off[2 * l + w];
+      if (!host[2 * l + w]) continue;
+      if (to_host) CK(cudaMemcpyAsync(host[2 * l + w], d, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+      else CK(cudaMemcpyAsync(d, host[2 * l + w], 4 * n, cudaMemcpyHostToDevice, c->stream));
+    }
+  }
+  return MEL_OK;
+}
+
+static int refresh_shadow(mel_ctx* c) {
+  if (c->cfg.precision == MEL_BF16)
+    to_bf16(c->d_p + c->off[2 * (c->L - 1)], c->d_shadow[c->shadow_cur], c->Npad * c->Klast, c->stream);
+  return check_launch(c, "shadow");
+}
+
+int mel_set_params(mel_ctx* c, const float* const* t) {
+  GUARD(c);
+  if (!t) return fail(c, MEL_EINVAL, "null tensors");
+  int r = copy_tensors(c, c->d_p, const_cast<float* const*>(t), false);
+  if (r) return r;
+  r = refresh_shadow(c);
+  if (r) return r;
+  CK(cudaStreamSynchronize(c->stream));
+  return MEL_OK;
+}
+
+int mel_get_params(mel_ctx* c, float* const* t) {
+  GUARD(c);
+  if (!t) return fail(c, MEL_EINVAL, "null tensors");
+  int r = copy_tensors(c, c->d_p, t, true);
+  if (r) return r;
+  CK(cudaStreamSynchronize(c->stream));
+  return MEL_OK;
+}
+
+int mel_get_state(mel_ctx* c, mel_state_view* s) {
+  GUARD(c);
+  if (!s) return fail(c, MEL_EINVAL, "null state");
+  int r;
+  if (s->p && (r = copy_tensors(c, c->d_p, s->p, true))) return r;
+  if (s->m && (r = copy_tensors(c, c->d_m, s->m, true))) return r;
+  if (s->v && (r = copy_tensors(c, c->d_v, s->v, true))) return r;
+  StepDev sd;
+  CK(cudaMemcpyAsync(&sd, c->d_sd, sizeof sd, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  s->adam_step = sd.k;
+  s->samples_seen = sd.S;
+  return MEL_OK;
+}
+
+int mel_set_state(mel_ctx* c, const mel_state_view* s) {
+  GUARD(c);
+  if (!s || !s->p || !s->m || !s->v) return fail(c, MEL_EINVAL, "null state");
+  int r;
+  if ((r = copy_tensors(c, c->d_p, s->p, false))) return r;
+  if ((r = copy_tensors(c, c->d_m, s->m, false))) return r;
+  if ((r = copy_tensors(c, c->d_v, s->v, false))) return r;
+  StepDev sd;
+  CK(cudaMemcpyAsync(&sd, c->d_sd, sizeof sd, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  sd.k = s->adam_step;
+  sd.S = s->samples_seen;
+  CK(cudaMemcpyAsync(c->d_sd, &sd, sizeof sd, cudaMemcpyHostToDevice, c->stream));
+  r = refresh_shadow(c);
+  if (r) return r;
+  CK(cudaStreamSynchronize(c->stream));
+  return MEL_OK;
+}
+
+int reservoir_put(mel_ctx* c, uint32_t sim, uint32_t t, const float X[5], const float* field, int on_device) {
+  GUARD(c);
+  if (!X || !field) return fail(c, MEL_EINVAL, "null X or field");
+  if (c->closed) return fail(c, MEL_ECLOSED, "reservoir_put after reservoir_close");
+  int r = ensure_ring_space(c);
+  if (r) return r;
+  const uint32_t S = c->cfg.staging_entries;
+  const uint32_t e = (uint32_t)(c->tail % S);
+  StMeta m{};
+  m.sim = sim; m.t = t;
+  for (int i = 0; i < 5; ++i) m.X[i] = X[i];
+  // the pinned metadata mirror entry may still be read by an earlier async copy
+  // of the same entry only if the ring wrapped, which ensure_ring_space excluded
+  c->h_stmeta[e] = m;
+  float* dst = const_cast<float*>(c->ra.st_field) + (uint64_t)e * c->Npad;
+  StMeta* dmeta = const_cast<StMeta*>(c->ra.st_meta) + e;
+  if (on_device) {
+    CK(cudaMemcpyAsync(dmeta, &c->h_stmeta[e], sizeof(StMeta), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dst, field, 4ull * c->N, cudaMemcpyDeviceToDevice, c->stream));
+  } else {
+    CK(cudaMemcpyAsync(dmeta, &c->h_stmeta[e], sizeof(StMeta), cudaMemcpyHostToDevice, c->copy_stream));
+    CK(cudaMemcpyAsync(dst, field, 4ull * c->N, cudaMemcpyHostToDevice, c->copy_stream));
+    CK(cudaEventRecord(c->ev_copy, c->copy_stream));
+    c->copy_pending = true;
+  }
+  c->tail += 1;
+  return MEL_OK;
+}
+
+int reservoir_close(mel_ctx* c) {
+  GUARD(c);
+  if (c->closed) return fail(c, MEL_EPROTO, "reservoir_close called twice");
+  c->closed = true;
+  return commit(c);
+}
+
+int reservoir_sample_batch(mel_ctx* c, int32_t* slots_host, uint32_t* n_host) {
+  GUARD(c);
+  int r = commit(c);
+  if (r) return r;
+  {
+    Timer t(c, MEL_K_SAMPLE, 1);
+    launch_sample(c->ra, c->d_slots, c->B, c->stream);
+  }
+  r = check_launch(c, "sample");
+  if (r) return r;
+  // During reception the fill phase never blocks (u <= p < C), so p = min(C, puts)
+  // at every commit point and the watermark gate is host-decidable.
+  bool need_sync = slots_host || n_host || c->closed;
+  uint32_t n = c->B;
+  if (!c->closed) {
+    const uint64_t p = c->tail < c->C ? c->tail : c->C;
+    if (p <= c->cfg.threshold) n = 0;
+  }
+  if (need_sync) {
+    r = sync_stream(c);
+    if (r) return r;
+    n = c->h_mirror->n_last;
+  }
+  c->batch_known = true;
+  c->batch_n = n;
+  if (n_host) *n_host = n;
+  if (slots_host && n) CK(cudaMemcpy(slots_host, c->d_slots, 4ull * n, cudaMemcpyDeviceToHost));
+  if (!c->closed && n == 0) return MEL_EAGAIN;
+  return MEL_OK;
+}
+
+int surrogate_step(mel_ctx* c, double* loss_host) {
+  GUARD(c);
+  const bool local_has = c->batch_known && c->batch_n > 0;
+  if (!c->batch_known) {
+    // no sample since the last step: this rank contributes nothing
+    CK(cudaMemsetAsync(&c->d_st->n_last, 0, 4, c->stream));
+    c->batch_n = 0;
+  }
+  int r;
+  {
+    Timer t(c, MEL_K_GATHER, 1);
+    launch_gather(c->ra, c->d_slots, c->B, c->cfg.steps_per_sim, c->d_xn, c->stream);
+  }
+  {
+    Timer t(c, MEL_K_HEAD_FWD, c->L - 1);
+    head_forward(c, c->d_xn, c->d_z, c->d_h, (int)c->B);
+  }
+  if ((r = check_launch(c, "head forward"))) return r;
+  r = c->cfg.precision == MEL_FP32 ? train_step_fp32(c) : train_step_bf16(c);
+  if (r) return r;
+  if ((r = head_backward(c))) return r;
+  if ((r = world_allreduce(c))) return r;
+  {
+    Timer t(c, MEL_K_LOSS, 1);
+    step_finalize(c->d_sd, (double)c->N, c->cfg.lr0, c->cfg.lr_min, c->cfg.lr_halving_samples, c->cfg.beta1,
+                  c->cfg.beta2, c->d_mirror, c->d_st, c->stream);
+  }
+  {
+    Timer t(c, MEL_K_ADAM, 1);
+    __nv_bfloat16* sh = nullptr;
+    uint64_t b0 = 0, b1 = 0;
+    if (c->cfg.precision == MEL_BF16) {
+      // the output-layer kernels of this step have completed (stream order), so
+      // the bf16 shadow is refreshed in place from the updated fp32 master
+      sh = c->d_shadow[0];
+      b0 = c->off[2 * (c->L - 1)];
+      b1 = b0 + c->Npad * c->Klast;
+    }
+    adam_flat(c->d_p, c->d_m, c->d_v, c->d_g, c->n_flat, c->d_sd, (float)c->cfg.beta1, (float)c->cfg.beta2,
+              (float)c->cfg.eps, sh, b0, b1, c->stream);
+  }
+  if ((r = check_launch(c, "adam"))) return r;
+  c->batch_known = false;
+  const bool need_sync = loss_host || !local_has || c->closed;
+  if (!need_sync) return MEL_OK;
+  if ((r = sync_stream(c))) return r;
+  const Mirror& m = *c->h_mirror;
+  if (m.status == 1) {
+    bool eos = c->closed && m.over && m.p == 0;
+    if (c->world > 1) {
+      // global EOS only when every rank is drained (reading Q11): n_total == 0 and
+      // every rank closed; ranks agree on n_total, so agree on closed too
+      int v = eos ? 1 : 0;
+      int* dv;
+      CK(cudaMalloc(&dv, 4));
+      CK(cudaMemcpy(dv, &v, 4, cudaMemcpyHostToDevice));
+      NK(ncclAllReduce(dv, dv, 1, ncclInt32, ncclMin, c->comm, c->stream));
+      CK(cudaMemcpyAsync(&v, dv, 4, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      cudaFree(dv);
+      eos = v == 1;
+    }
+    return eos ? MEL_EOS : MEL_EAGAIN;
+  }
+  if (loss_host) *loss_host = m.loss;
+  if (!std::isfinite(m.loss)) return fail(c, MEL_ENONFINITE, "loss is not finite (%g)", m.loss);
+  return MEL_OK;
+}
+
+int surrogate_eval(mel_ctx* c, const float* X, const uint32_t* t, const float* fields, uint32_t n, double* mse,
+                   float* pred) {
+  GUARD(c);
+  if (!X || !t || n == 0) return fail(c, MEL_EINVAL, "bad eval arguments");
+  const uint32_t chunk = c->B;
+  if (!c->d_eval_x) {
+    DALLOC(c->d_eval_x, (size_t)chunk * 5); DALLOC(c->d_eval_t, chunk); DALLOC(c->d_eval_xn, (size_t)chunk * 8);
+    DALLOC(c->d_eval_y, (size_t)chunk * c->Npad); DALLOC(c->d_eval_f, (size_t)chunk * c->N);
+    for (int l = 0; l < c->L - 1; ++l) {
+      DALLOC(c->d_eval_z[l], (size_t)chunk * c->dims[l + 1]);
+      DALLOC(c->d_eval_h[l], (size_t)chunk * c->dims[l + 1]);
+    }
+  }
+  double* d_part;
+  DALLOC(d_part, 256);
+  double total = 0.0;
+  const float lo = c->cfg.temp_lo, span = c->cfg.temp_hi - c->cfg.temp_lo;
+  std::vector<double> parts(256);
+  for (uint32_t s0 = 0; s0 < n; s0 += chunk) {
+    const uint32_t m = (n - s0) < chunk ? (n - s0) : chunk;
+    CK(cudaMemcpyAsync(c->d_eval_x, X + 5ull * s0, 20ull * m, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_eval_t, t + s0, 4ull * m, cudaMemcpyHostToDevice, c->stream));
+    eval_inputs(c->d_eval_x, c->d_eval_t, (int)m, c->cfg.steps_per_sim, lo, span, c->d_eval_xn, c->stream);
+    head_forward(c, c->d_eval_xn, c->d_eval_z, c->d_eval_h, (int)m);
+    const int L = c->L;
+    sgemm(false, true, (int)m, (int)c->N, (int)c->Klast, c->d_eval_h[L - 2], (int)c->Klast, c->d_p + c->off[2 * (L - 1)],
+          (int)c->Klast, c->d_eval_y, (int)c->Npad, EPI_BIAS, c->d_p + c->off[2 * (L - 1) + 1], nullptr, 0, 1, c->stream);
+    c->launches += 2 + (L - 1) + 1;
+    if (fields) {
+      CK(cudaMemcpyAsync(c->d_eval_f, fields + (uint64_t)s0 * c->N, 4ull * m * c->N, cudaMemcpyHostToDevice, c->stream));
+      normalise_fields(c->d_eval_f, c->d_eval_f, (uint64_t)m * c->N, lo, span, c->stream);
+      const int np = eval_mse_partial(c->d_eval_y, c->d_eval_f, (int)m, (int)c->N, (int)c->Npad, d_part, c->stream);
+      c->launches += 2;
+      CK(cudaMemcpyAsync(parts.data(), d_part, 8ull * np, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      for (int i = 0; i < np; ++i) total += parts[i];
+    }
+    if (pred) {
+      std::vector<float> y((size_t)m * c->Npad);
+      CK(cudaMemcpyAsync(y.data(), c->d_eval_y, 4ull * m * c->Npad, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      for (uint32_t i = 0; i < m; ++i)
+        for (uint32_t j = 0; j < c->N; ++j) pred[(uint64_t)(s0 + i) * c->N + j] = y[(size_t)i * c->Npad + j] * span + lo;
+    }
+  }
+  int r = check_launch(c, "eval");
+  cudaFree(d_part);
+  if (r) return r;
+  CK(cudaStreamSynchronize(c->stream));
+  if (mse) *mse = fields ? total / ((double)n * c->N) : NAN;
+  return MEL_OK;
+}
+
+int reservoir_stats(mel_ctx* c, mel_stats* out) {
+  GUARD(c);
+  if (!out) return fail(c, MEL_EINVAL, "null stats");
+  int r = sync_stream(c);
+  if (r) return r;
+  ResDev st;
+  StepDev sd;
+  CK(cudaMemcpy(&st, c->d_st, sizeof st, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&sd, c->d_sd, sizeof sd, cudaMemcpyDeviceToHost));
+  memset(out, 0, sizeof *out);
+  out->population = st.p; out->unseen = st.u; out->seen = st.p - st.u;
+  out->puts = c->tail; out->committed = st.q; out->draws = st.d; out->evictions = st.evictions;
+  out->pending = c->tail - st.consumed;
+  out->steps = sd.k; out->samples = sd.S;
+  for (int i = 0; i < MEL_HIST_BINS; ++i) out->hist[i] = st.hist[i];
+  out->over = st.over; out->closed = c->closed;
+  out->last_loss = sd.loss;
+  return MEL_OK;
+}
+
+int reservoir_dump(mel_ctx* c, uint32_t* sim, uint32_t* t, float* X, uint32_t* seen, uint64_t* put_seq, void* payload) {
+  GUARD(c);
+  int r = sync_stream(c);
+  if (r) return r;
+  const uint32_t C = c->C;
+  if (sim || t || X) {
+    std::vector<SlotMeta> m(C);
+    CK(cudaMemcpy(m.data(), c->ra.meta, sizeof(SlotMeta) * C, cudaMemcpyDeviceToHost));
+    for (uint32_t i = 0; i < C; ++i) {
+      if (sim) sim[i] = m[i].sim;
+      if (t) t[i] = m[i].t;
+      if (X) for (int k = 0; k < 5; ++k) X[5 * i + k] = m[i].X[k];
+    }
+  }
+  if (seen) CK(cudaMemcpy(seen, c->ra.seen, 4ull * C, cudaMemcpyDeviceToHost));
+  if (put_seq) CK(cudaMemcpy(put_seq, c->ra.put_seq, 8ull * C, cudaMemcpyDeviceToHost));
+  if (payload) {
+    const size_t esz = c->cfg.storage == MEL_STORE_F32 ? 4 : 2;
+    CK(cudaMemcpy2D(payload, esz * c->N, c->ra.payload, esz * c->Npad, esz * c->N, C, cudaMemcpyDeviceToHost));
+  }
+  return MEL_OK;
+}
+
+int mel_sync(mel_ctx* c) {
+  GUARD(c);
+  return sync_stream(c);
+}
+
+int mel_kernel_time(mel_ctx* c, int k, double* ms, uint64_t* launches) {
+  GUARD(c);
+  if (k < 0 || k >= MEL_K_COUNT) return fail(c, MEL_EINVAL, "bad kernel id");
+  int r = sync_stream(c);
+  if (r) return r;
+  drain_timers(c);
+  if (ms) *ms = c->kms[k];
+  if (launches) *launches = c->klaunch[k];
+  return MEL_OK;
+}
+
+int mel_kernel_time_reset(mel_ctx* c) {
+  GUARD(c);
+  int r = sync_stream(c);
+  if (r) return r;
+  drain_timers(c);
+  for (int k = 0; k < MEL_K_COUNT; ++k) { c->kms[k] = 0; c->klaunch[k] = 0; }
+  return MEL_OK;
+}
+
+int mel_launch_count(const mel_ctx* c, uint64_t* n) {
+  if (!c || !n) return MEL_EINVAL;
+  *n = c->launches;
+  return MEL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,377 @@
+// SIMT (FFMA) kernels of the surrogate trainer: the head layers (6 -> 256 ->
+// 256, 0.03% of the step FLOPs at paper shape), the fp32 parity mode of
+// the output layer, deterministic reductions, Adam and Philox
+// init.  The tensor-core output layer (bf16 mode) lives in tc_out.cu.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mel {
+
+namespace {
+
+constexpr int TM = 64, TN = 64, TK = 16;
+
+// C[M][N] = sum_k A(m,k) B(k,n);  A(m,k) = TA ? A[k*lda+m] : A[m*lda+k];
+// B(k,n) = TB ? B[n*ldb+k] : B[k*ldb+n].  gridDim.z = split-K partitions; with
+// splits > 1, C points at the partial buffer [z][M][ldc].
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256)
+sgemm_kernel(int M, int N, int K, const float* __restrict__ A, int lda, const float* __restrict__ B, int ldb,
+             float* __restrict__ C, int ldc, int epi, const float* __restrict__ bias, float* __restrict__ H, int ldh,
+             int k_chunk) {
+  __shared__ float As[TK][TM + 4];
+  __shared__ float Bs[TK][TN + 4];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
+  const int kb = blockIdx.z * k_chunk;
+  const int ke = min(K, kb + k_chunk);
+  float acc[4][4] = {};
+  for (int k0 = kb; k0 < ke; k0 += TK) {
+    // A tile: 64 x 16
+    for (int i = threadIdx.x; i < TM * TK; i += 256) {
+      int mm, kk;
+      if (TA) { mm = i % TM; kk = i / TM; } else { kk = i % TK; mm = i / TK; }
+      const int gm = m0 + mm, gk = k0 + kk;
+      float v = 0.f;
+      if (gm < M && gk < ke) v = TA ? A[(size_t)gk * lda + gm] : A[(size_t)gm * lda + gk];
+      As[kk][mm] = v;
+    }
+    for (int i = threadIdx.x; i < TN * TK; i += 256) {
+      int nn, kk;
+      if (TB) { kk = i % TK; nn = i / TK; } else { nn = i % TN; kk = i / TN; }
+      const int gn = n0 + nn, gk = k0 + kk;
+      float v = 0.f;
+      if (gn < N && gk < ke) v = TB ? B[(size_t)gn * ldb + gk] : B[(size_t)gk * ldb + gn];
+      Bs[kk][nn] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  float* Cz = C + (size_t)blockIdx.z * M * ldc;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty + 16 * i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx + 16 * j;
+      if (n >= N) continue;
+      float v = acc[i][j];
+      if (epi != EPI_STORE) v += bias[n];
+      Cz[(size_t)m * ldc + n] = v;
+      if (epi == EPI_BIAS_RELU) H[(size_t)m * ldh + n] = fmaxf(v, 0.f);
+    }
+  }
+}
+
+__global__ void splitk_reduce_kernel(int M, int N, int splits, const float* __restrict__ part, float* __restrict__ C,
+                                     int ldc, const float* __restrict__ mask, int ldm) {
+  const size_t total = (size_t)M * N;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i / N), n = (int)(i % N);
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += part[(size_t)z * M * N + i];   // fixed order
+    if (mask && !(mask[(size_t)m * ldm + n] > 0.f)) s = 0.f;             // ReLU'(0) = 0
+    C[(size_t)m * ldc + n] = s;
+  }
+}
+
+// Output layer, fp32 parity mode: Y = H W^T + b, raw gradient dS/dY = 2 (Y - T)
+// for valid rows/cols (0 elsewhere), SSE partial per block.
+__global__ void __launch_bounds__(256)
+out_fwd_f32_kernel(OutArgs a) {
+  __shared__ float As[TK][TM + 4];
+  __shared__ float Bs[TK][TN + 4];
+  __shared__ double s_red[256];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
+  const int M = a.B, K = a.K;
+  const int Nn = (int)a.Npad;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += TK) {
+    for (int i = threadIdx.x; i < TM * TK; i += 256) {
+      const int kk = i % TK, mm = i / TK, gm = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gm < M && gk < K) ? a.H[(size_t)gm * a.ldh + gk] : 0.f;
+    }
+    for (int i = threadIdx.x; i < TN * TK; i += 256) {
+      const int kk = i % TK, nn = i / TK, gn = n0 + nn, gk = k0 + kk;
+      Bs[kk][nn] = (gn < Nn && gk < K) ? a.W[(size_t)gn * K + gk] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  const uint32_t n_valid = a.st->n_last;
+  double sse = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty + 16 * i;
+    if (m >= M) continue;
+    const bool row_ok = (uint32_t)m < n_valid;
+    const int32_t slot = row_ok ? a.slots[m] : 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx + 16 * j;
+      if (n >= Nn) continue;
+      float g = 0.f;
+      if (row_ok && (uint32_t)n < a.N) {
+        const float y = acc[i][j] + a.b[n];
+        const size_t off = (size_t)slot * a.Npad + n;
+        const float t = a.storage == 0 ? static_cast<const float*>(a.payload)[off]
+                                       : bf16_bits_to_f32(static_cast<const uint16_t*>(a.payload)[off]);
+        const float r = y - t;
+        sse += (double)r * (double)r;
+        g = 2.f * r;
+      }
+      a.dY[(size_t)m * a.Npad + n] = g;
+    }
+  }
+  s_red[threadIdx.x] = sse;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s_red[threadIdx.x] += s_red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a.sse_part[blockIdx.y * gridDim.x + blockIdx.x] = s_red[0];
+}
+
+__global__ void col_sum_kernel(const float* __restrict__ X, int rows, int cols, int ld, float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  float s = 0.f;
+  for (int r = 0; r < rows; ++r) s += X[(size_t)r * ld + c];   // fixed order over the batch
+  out[c] = s;
+}
+
+__global__ void reduce_local_kernel(StepDev* sd, const double* parts, int n_parts, const ResDev* st) {
+  __shared__ double s[256];
+  double v = 0.0;
+  for (int i = threadIdx.x; i < n_parts; i += 256) v += parts[i];
+  s[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { sd->red[0] = s[0]; sd->red[1] = (double)st->n_last; }
+}
+
+__global__ void step_finalize_kernel(StepDev* sd, double n_field, double lr0, double lr_min, uint64_t halving,
+                                     double b1, double b2, Mirror* mirror, ResDev* st) {
+  const double sse = sd->red[0], n = sd->red[1];
+  st->n_last = 0;                       // a batch is consumed by exactly one step
+  mirror->n_last = 0;
+  if (n <= 0.0) {
+    sd->skip = 1;
+    mirror->status = 1; mirror->n_total = 0.0;
+    return;
+  }
+  sd->skip = 0;
+  const double denom = n_field * n;
+  sd->loss = sse / denom;
+  sd->nonfinite = !isfinite(sd->loss);
+  sd->scale = (float)(1.0 / denom);
+  // lr halved every `halving` global samples, floor lr_min (reading Q24)
+  const uint64_t S = sd->S;
+  const double lr = fmax(lr_min, lr0 * exp2(-(double)(S / halving)));
+  const uint64_t k = sd->k + 1;
+  sd->lr = (float)lr;
+  sd->c1 = (float)(1.0 - pow(b1, (double)k));
+  sd->c2 = (float)(1.0 - pow(b2, (double)k));
+  sd->k = k;
+  sd->S = S + (uint64_t)n;
+  mirror->status = 0; mirror->loss = sd->loss; mirror->n_total = n;
+  mirror->adam_k = k; mirror->samples = sd->S;
+}
+
+// Adam (bias-corrected), flat over every tensor; g is the raw dS/dtheta and is
+// scaled by 1/(N * n_total) here.  Writes the bf16 shadow of [sh_begin, sh_end).
+__global__ void __launch_bounds__(256)
+adam_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v, const float* __restrict__ g,
+            uint64_t n4, const StepDev* __restrict__ sd, float b1, float b2, float eps,
+            __nv_bfloat16* __restrict__ shadow, uint64_t sh_begin, uint64_t sh_end) {
+  if (sd->skip) return;
+  const float scale = sd->scale, lr = sd->lr, c1 = sd->c1, c2 = sd->c2;
+  const float ib1 = 1.f - b1, ib2 = 1.f - b2;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4; i += (uint64_t)gridDim.x * blockDim.x) {
+    float4 pp = reinterpret_cast<float4*>(p)[i];
+    float4 mm = reinterpret_cast<float4*>(m)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    const float4 gg = reinterpret_cast<const float4*>(g)[i];
+    float* P = &pp.x; float* Mv = &mm.x; float* V = &vv.x; const float* G = &gg.x;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float gr = G[c] * scale;
+      Mv[c] = b1 * Mv[c] + ib1 * gr;
+      V[c] = b2 * V[c] + ib2 * gr * gr;
+      const float mh = Mv[c] / c1;
+      const float vh = V[c] / c2;
+      P[c] = P[c] - lr * mh / (sqrtf(vh) + eps);
+    }
+    reinterpret_cast<float4*>(p)[i] = pp;
+    reinterpret_cast<float4*>(m)[i] = mm;
+    reinterpret_cast<float4*>(v)[i] = vv;
+    const uint64_t e = 4 * i;
+    if (shadow && e >= sh_begin && e < sh_end) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(P[0], P[1]);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(P[2], P[3]);
+      uint2 pk = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+      reinterpret_cast<uint2*>(shadow + (e - sh_begin))[0] = pk;
+    }
+  }
+}
+
+__global__ void init_kernel(float* dst, uint64_t count, uint32_t tid, uint32_t fan_in, uint64_t seed) {
+  const double a = 1.0 / sqrt((double)fan_in);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
+    const double u = unit_double(philox_r64(seed, TAG_INIT, i, tid));
+    dst[i] = (float)((2.0 * u - 1.0) * a);     // fp64 then RNE to fp32 (reading Q22)
+  }
+}
+
+__global__ void to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+__global__ void relu_mask_kernel(float* X, const float* Z, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    if (!(Z[i] > 0.f)) X[i] = 0.f;
+}
+
+__global__ void eval_mse_kernel(const float* __restrict__ Y, const float* __restrict__ T, int rows, int cols, int ld,
+                                double* part) {
+  __shared__ double s[256];
+  double acc = 0.0;
+  const size_t total = (size_t)rows * cols;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / cols, c = i % cols;
+    const double d = (double)Y[r * ld + c] - (double)T[r * cols + c];
+    acc += d * d;
+  }
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = s[0];
+}
+
+__global__ void eval_inputs_kernel(const float* X, const uint32_t* t, int n, uint32_t tau, float lo, float span,
+                                   float* xn) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  float o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int c = 0; c < 5; ++c) o[c] = normalise_rn(X[b * 5 + c], lo, span);
+  o[5] = __fdiv_rn((float)t[b], (float)tau);
+  for (int c = 0; c < 8; ++c) xn[b * 8 + c] = o[c];
+}
+
+__global__ void normalise_kernel(const float* src, float* dst, uint64_t n, float lo, float span) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = normalise_rn(src[i], lo, span);
+}
+
+inline unsigned grid_for(uint64_t n, unsigned block = 256, unsigned cap = 148 * 16) {
+  uint64_t g = (n + block - 1) / block;
+  if (g > cap) g = cap;
+  if (g == 0) g = 1;
+  return (unsigned)g;
+}
+
+}  // namespace
+
+void sgemm(bool ta, bool tb, int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
+           int ldc, int epi, const float* bias, float* H, int ldh, int splits, cudaStream_t s) {
+  if (splits < 1) splits = 1;
+  int k_chunk = (K + splits - 1) / splits;
+  k_chunk = ((k_chunk + TK - 1) / TK) * TK;
+  dim3 grid((N + TN - 1) / TN, (M + TM - 1) / TM, splits);
+  if (!ta && !tb) sgemm_kernel<false, false><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk);
+  else if (!ta && tb) sgemm_kernel<false, true><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk);
+  else if (ta && !tb) sgemm_kernel<true, false><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk);
+  else sgemm_kernel<true, true><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk);
+}
+
+void splitk_reduce(int M, int N, int splits, const float* part, float* C, int ldc, const float* relu_mask, int ldm,
+                   cudaStream_t s) {
+  splitk_reduce_kernel<<<grid_for((uint64_t)M * N), 256, 0, s>>>(M, N, splits, part, C, ldc, relu_mask, ldm);
+}
+
+int out_fwd_f32(const OutArgs& a, cudaStream_t s) {
+  dim3 grid((unsigned)((a.Npad + TN - 1) / TN), (a.B + TM - 1) / TM);
+  out_fwd_f32_kernel<<<grid, 256, 0, s>>>(a);
+  return (int)(grid.x * grid.y);
+}
+
+void col_sum(const float* X, int rows, int cols, int ld, float* out, cudaStream_t s) {
+  col_sum_kernel<<<(cols + 255) / 256, 256, 0, s>>>(X, rows, cols, ld, out);
+}
+
+void reduce_local(StepDev* sd, const double* parts, int n_parts, const ResDev* st, cudaStream_t s) {
+  reduce_local_kernel<<<1, 256, 0, s>>>(sd, parts, n_parts, st);
+}
+
+void step_finalize(StepDev* sd, double n_field, double lr0, double lr_min, uint64_t halving, double b1, double b2,
+                   Mirror* mirror, ResDev* st, cudaStream_t s) {
+  step_finalize_kernel<<<1, 1, 0, s>>>(sd, n_field, lr0, lr_min, halving, b1, b2, mirror, st);
+}
+
+void adam_flat(float* p, float* m, float* v, const float* g, uint64_t n, const StepDev* sd, float b1, float b2,
+               float eps, __nv_bfloat16* shadow, uint64_t sh_begin, uint64_t sh_end, cudaStream_t s) {
+  const uint64_t n4 = n / 4;   // the flat buffer is padded to a multiple of 4
+  adam_kernel<<<grid_for(n4, 256, 148 * 8), 256, 0, s>>>(p, m, v, g, n4, sd, b1, b2, eps, shadow, sh_begin, sh_end);
+}
+
+void init_tensor(float* dst, uint64_t count, uint32_t tid, uint32_t fan_in, uint64_t seed, cudaStream_t s) {
+  init_kernel<<<grid_for(count), 256, 0, s>>>(dst, count, tid, fan_in, seed);
+}
+
+void to_bf16(const float* src, __nv_bfloat16* dst, uint64_t n, cudaStream_t s) {
+  to_bf16_kernel<<<grid_for(n), 256, 0, s>>>(src, dst, n);
+}
+
+void relu_mask_mul(float* X, const float* Z, uint64_t n, cudaStream_t s) {
+  relu_mask_kernel<<<grid_for(n), 256, 0, s>>>(X, Z, n);
+}
+
+int eval_mse_partial(const float* Y, const float* T, int rows, int cols, int ld, double* part, cudaStream_t s) {
+  const unsigned g = grid_for((uint64_t)rows * cols, 256, 256);
+  eval_mse_kernel<<<g, 256, 0, s>>>(Y, T, rows, cols, ld, part);
+  return (int)g;
+}
+
+void eval_inputs(const float* X, const uint32_t* t, int n, uint32_t tau, float lo, float span, float* xn,
+                 cudaStream_t s) {
+  eval_inputs_kernel<<<(n + 127) / 128, 128, 0, s>>>(X, t, n, tau, lo, span, xn);
+}
+
+void normalise_fields(const float* src, float* dst, uint64_t n, float lo, float span, cudaStream_t s) {
+  normalise_kernel<<<grid_for(n), 256, 0, s>>>(src, dst, n, lo, span);
+}
+
+}  // namespace mel

@@ -1,0 +1,286 @@
+// Reservoir kernels (Algorithm 1) in the
+// deterministic op-log form of DESIGN.md (readings R1-R9):
+//   commit_ctrl  : one control CTA applies the pending puts in FIFO order under
+//                  the put rule: fill phase slot = p + lane prefix;
+//                  full phase evicts the r-th *seen* slot (r from Philox EVICT(q)),
+//                  found by a block-wide rank-select over the seen bitmap in SMEM;
+//                  stops when every slot is unseen (P:264 back-pressure).
+//   commit_copy  : data plane, one CTA row per committed put, 16-byte vector
+//                  loads of the fp32 staging entry, normalised on the fly and
+//                  stored as fp32 or bf16 (P:210 wire data, reading R8).
+//   sample_kernel: B Philox SAMPLE(d+b) draws with replacement,
+//                  seen counters by atomicAdd (order-free), u -= #(0->1); after
+//                  the reception is over, sequential DRAIN draws with removal.
+//   gather_inputs: normalised network inputs (X, t) of the batch (reading Q13).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mel {
+
+namespace {
+
+constexpr int CTRL_THREADS = 1024;
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  return v;
+}
+
+// exclusive block scan of one value per thread (CTRL_THREADS threads)
+__device__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t incl = warp_incl_scan(v);
+  if (lane == 31) s_warp[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t x = (lane < (int)(blockDim.x >> 5)) ? s_warp[lane] : 0u;
+    uint32_t xi = warp_incl_scan(x);
+    s_warp[lane] = xi - x;
+  }
+  __syncthreads();
+  uint32_t r = s_warp[w] + incl - v;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(CTRL_THREADS, 1)
+commit_ctrl(ResArgs a, uint64_t tail, uint32_t closed) {
+  extern __shared__ uint32_t s_bits[];          // seen bitmap, ceil(C/32) words
+  __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_cmd[4];                  // 0: mode (0 stop, 1 fill, 2 evict), 1: count / r, 2: result slot
+  const uint32_t W = (a.C + 31) / 32;
+  for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) s_bits[i] = a.bitmap[i];
+  ResDev* st = a.st;
+  uint32_t p = st->p, u = st->u;
+  uint64_t q = st->q, consumed = st->consumed;
+  uint32_t n_plan = 0;
+  __syncthreads();
+  const uint32_t wpt = (W + blockDim.x - 1) / blockDim.x;   // words per thread
+  while (true) {
+    if (threadIdx.x == 0) {
+      if (consumed >= tail || u == a.C) {
+        s_cmd[0] = 0;                                        // P:264 "wait"
+      } else if (p < a.C) {
+        uint64_t avail = tail - consumed;
+        const uint64_t room = (uint64_t)(a.C - p);
+        const uint32_t cnt = (uint32_t)(avail < room ? avail : room);
+        s_cmd[0] = 1; s_cmd[1] = cnt;
+      } else {
+        uint32_t s = p - u;                                  // seen population
+        s_cmd[0] = 2;
+        s_cmd[1] = bounded(philox_r64(a.seed, TAG_EVICT, q, a.rank), s);
+      }
+    }
+    __syncthreads();
+    const uint32_t mode = s_cmd[0];
+    if (mode == 0) break;
+    if (mode == 1) {
+      // fill phase: dense prefix, slot = p + i (deterministic lane prefix)
+      const uint32_t cnt = s_cmd[1];
+      for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+        const uint32_t j = p + i;
+        const uint32_t e = (uint32_t)((consumed + i) % a.S);
+        a.meta[j] = a.st_meta[e];
+        a.seen[j] = 0;
+        a.put_seq[j] = q + i;
+        a.plan[n_plan + i] = make_uint2(e, j);
+      }
+      p += cnt; u += cnt; q += cnt; consumed += cnt; n_plan += cnt;
+      __syncthreads();
+      continue;
+    }
+    // full phase: find the r-th set bit (ascending slot id) of the seen bitmap
+    const uint32_t r = s_cmd[1];
+    uint32_t cnt = 0;
+    const uint32_t w0 = threadIdx.x * wpt;
+    for (uint32_t k = 0; k < wpt; ++k)
+      if (w0 + k < W) cnt += __popc(s_bits[w0 + k]);
+    const uint32_t before = block_excl_scan(cnt, s_warp);
+    if (r >= before && r < before + cnt) {
+      uint32_t rem = r - before;
+      for (uint32_t k = 0; k < wpt; ++k) {
+        uint32_t word = s_bits[w0 + k];
+        uint32_t pc = __popc(word);
+        if (rem < pc) {
+          for (uint32_t b = 0; b < 32; ++b) {
+            if (word & (1u << b)) {
+              if (rem == 0) { s_cmd[2] = (w0 + k) * 32 + b; break; }
+              --rem;
+            }
+          }
+          break;
+        }
+        rem -= pc;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t j = s_cmd[2];
+      const uint32_t e = (uint32_t)(consumed % a.S);
+      const uint32_t sc = a.seen[j];
+      st->hist[sc < HIST_BINS ? sc : HIST_BINS - 1] += 1;     // retired with its count
+      st->evictions += 1;
+      s_bits[j >> 5] &= ~(1u << (j & 31));
+      a.meta[j] = a.st_meta[e];
+      a.seen[j] = 0;
+      a.put_seq[j] = q;
+      a.plan[n_plan] = make_uint2(e, j);
+    }
+    q += 1; u += 1; consumed += 1; n_plan += 1;
+    __syncthreads();
+  }
+  for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) a.bitmap[i] = s_bits[i];
+  if (threadIdx.x == 0) {
+    st->p = p; st->u = u; st->q = q; st->consumed = consumed; st->n_plan = n_plan;
+    if (closed && consumed == tail) st->over = 1;
+    Mirror* m = a.mirror;
+    m->consumed = consumed; m->q = q; m->p = p; m->u = u; m->over = st->over;
+    m->evictions = st->evictions; m->d = st->d;
+  }
+}
+
+// data plane: blockIdx.y = plan index, 4 floats per thread per iteration
+template <int STORAGE>
+__global__ void __launch_bounds__(256)
+commit_copy(ResArgs a) {
+  const uint32_t y = blockIdx.y;
+  if (y >= a.st->n_plan) return;
+  const uint2 ej = a.plan[y];
+  const float4* src = reinterpret_cast<const float4*>(a.st_field + (uint64_t)ej.x * a.Npad);
+  const uint32_t n4 = (a.N + 3) / 4;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+    float4 v = __ldg(src + i);
+    float o[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) o[c] = (4 * i + c < a.N) ? normalise_rn(o[c], a.lo, a.span) : 0.f;
+    if (STORAGE == 0) {
+      float4* dst = reinterpret_cast<float4*>(static_cast<float*>(a.payload) + (uint64_t)ej.y * a.Npad);
+      dst[i] = make_float4(o[0], o[1], o[2], o[3]);
+    } else {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(o[0], o[1]);   // RNE
+      __nv_bfloat162 hi = __floats2bfloat162_rn(o[2], o[3]);
+      uint2 pk = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+      uint2* dst = reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.payload) + (uint64_t)ej.y * a.Npad);
+      dst[i] = pk;
+    }
+  }
+}
+
+constexpr int SAMPLE_THREADS = 1024;
+
+__global__ void __launch_bounds__(SAMPLE_THREADS, 1)
+sample_kernel(ResArgs a, int32_t* slots, uint32_t B) {
+  __shared__ uint32_t s_cnt;
+  ResDev* st = a.st;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  const uint32_t p = st->p;
+  const uint64_t d = st->d;
+  if (!st->over) {
+    if (p <= a.theta) {                          // P:242 watermark gate
+      if (threadIdx.x == 0) { st->n_last = 0; a.mirror->n_last = 0; }
+      return;
+    }
+    uint32_t local = 0;
+    for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) {
+      const uint32_t i = bounded(philox_r64(a.seed, TAG_SAMPLE, d + b, a.rank), p);
+      slots[b] = (int32_t)i;
+      const uint32_t old = atomicAdd(&a.seen[i], 1u);
+      if (old == 0) { ++local; atomicOr(&a.bitmap[i >> 5], 1u << (i & 31)); }
+    }
+    if (local) atomicAdd(&s_cnt, local);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      st->u -= s_cnt;
+      st->d = d + B;
+      st->n_last = B;
+      Mirror* m = a.mirror;
+      m->u = st->u; m->d = st->d; m->n_last = B; m->p = p; m->over = 0;
+    }
+    return;
+  }
+  // drain (P:249-258 with is_reception_over): sequential, each draw removes its item
+  if (threadIdx.x == 0) {
+    uint32_t pp = p, n = 0, u = st->u;
+    uint64_t dd = d;
+    while (n < B && pp > 0) {
+      const uint32_t k = bounded(philox_r64(a.seed, TAG_DRAIN, dd, a.rank), pp);
+      ++dd;
+      const uint32_t j = a.pos[k];
+      const uint32_t sc = a.seen[j];
+      if (sc == 0) --u;
+      a.seen[j] = sc + 1;
+      st->hist[sc + 1 < HIST_BINS ? sc + 1 : HIST_BINS - 1] += 1;
+      slots[n++] = (int32_t)j;
+      a.pos[k] = a.pos[pp - 1];
+      --pp;
+    }
+    st->p = pp; st->u = u; st->d = dd; st->n_last = n;
+    Mirror* m = a.mirror;
+    m->p = pp; m->u = u; m->d = dd; m->n_last = n; m->over = 1;
+  }
+}
+
+__global__ void gather_inputs(ResArgs a, const int32_t* slots, uint32_t B, uint32_t tau, float* xn) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const uint32_t n = a.st->n_last;
+  float out[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (b < n) {
+    const SlotMeta m = a.meta[slots[b]];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) out[c] = normalise_rn(m.X[c], a.lo, a.span);
+    out[5] = __fdiv_rn((float)m.t, (float)tau);
+  }
+  float4* dst = reinterpret_cast<float4*>(xn + (uint64_t)b * 8);
+  dst[0] = make_float4(out[0], out[1], out[2], out[3]);
+  dst[1] = make_float4(out[4], out[5], out[6], out[7]);
+}
+
+__global__ void init_res(ResArgs a) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.C; i += gridDim.x * blockDim.x) {
+    a.pos[i] = i;
+    a.seen[i] = 0;
+    a.put_seq[i] = ~0ull;
+    SlotMeta m; m.sim = 0xFFFFFFFFu; m.t = 0xFFFFFFFFu;
+    for (int c = 0; c < 5; ++c) m.X[c] = 0.f;
+    m.pad = 0;
+    a.meta[i] = m;
+  }
+}
+
+}  // namespace
+
+void launch_commit(const ResArgs& a, uint64_t tail, uint32_t closed, uint32_t max_entries, cudaStream_t s) {
+  const uint32_t W = (a.C + 31) / 32;
+  const size_t smem = (size_t)W * 4;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(commit_ctrl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  commit_ctrl<<<1, CTRL_THREADS, smem, s>>>(a, tail, closed);
+  if (max_entries == 0) return;
+  const uint32_t n4 = (a.N + 3) / 4;
+  uint32_t gx = (n4 + 255) / 256;
+  if (gx > 512) gx = 512;
+  dim3 grid(gx, max_entries);
+  if (a.storage == 0) commit_copy<0><<<grid, 256, 0, s>>>(a);
+  else commit_copy<1><<<grid, 256, 0, s>>>(a);
+}
+
+void launch_sample(const ResArgs& a, int32_t* slots, uint32_t B, cudaStream_t s) {
+  sample_kernel<<<1, SAMPLE_THREADS, 0, s>>>(a, slots, B);
+}
+
+void launch_gather(const ResArgs& a, const int32_t* slots, uint32_t B, uint32_t tau, float* xn, cudaStream_t s) {
+  gather_inputs<<<(B + 127) / 128, 128, 0, s>>>(a, slots, B, tau, xn);
+}
+
+void launch_init_res(const ResArgs& a, cudaStream_t s) {
+  init_res<<<256, 256, 0, s>>>(a);
+}
+
+}  // namespace mel

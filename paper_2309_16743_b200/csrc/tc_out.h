@@ -1,0 +1,55 @@
+// Tensor-core (tcgen05 / TMEM / TMA) output layer of the surrogate, bf16 mode.
+// See tc_out.cu and DESIGN.md "Kernels".
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.h"
+
+namespace mel {
+namespace tc {
+
+struct TcBuffers {
+  __nv_bfloat16* h_bf16 = nullptr;   // [B][K] last hidden activations (bf16)
+  __nv_bfloat16* dyT = nullptr;      // [Npad][B] dS/dY transposed (bf16)
+  void* maps = nullptr;              // device copy of the TMA descriptors
+  void* h_maps = nullptr;            // host copies (CUtensorMap)
+  uint64_t Npad = 0;
+  uint32_t B = 0, K = 0;
+  int dh_splits = 0;
+  int fwd_ctas = 0;
+};
+
+struct OutTcArgs {
+  uint32_t N, B, K;
+  uint64_t Npad;
+  const __nv_bfloat16* w_bf16;       // [Npad][K] shadow of W_L
+  const float* b;                    // [Npad] b_L
+  const __nv_bfloat16* h_bf16;       // [B][K]
+  const __nv_bfloat16* payload;      // reservoir slots [C][Npad] bf16 (normalised)
+  const int32_t* slots;              // [B]
+  const ResDev* st;                  // n_valid = st->n_last
+  __nv_bfloat16* dyT;                // out: [Npad][B]
+  float* gW;                         // out: raw dS/dW_L [Npad][K]
+  float* gb;                         // out: raw dS/db_L [Npad]
+  double* sse_part;                  // out: per-CTA SSE partials
+  float* dh_part;                    // scratch: split-K partials of dS/dH
+  float* dz;                         // out: dS/dZ_{L-1} [B][K]
+  const float* z;                    // Z_{L-1} [B][K] (ReLU mask)
+};
+
+int alloc_buffers(TcBuffers& t, uint64_t Npad, uint32_t B, uint32_t K);
+void free_buffers(TcBuffers& t);
+int prepare(TcBuffers& t, uint64_t Npad, uint32_t B, uint32_t K,
+            const __nv_bfloat16* w_bf16);   // TMA descriptors, kernel attributes
+size_t dh_part_elems(uint32_t B, uint32_t K);
+int max_sse_parts(uint64_t Npad);
+// forward + MSE gradient + dW_L/db_L (per 128-row tile of W_L); returns #SSE partials
+int launch_out_fwd_dw(const OutTcArgs& a, const TcBuffers& t, cudaStream_t s);
+// dS/dH = dY W_L (split-K over N) then the ReLU' mask -> dz
+void launch_out_dh(const OutTcArgs& a, const TcBuffers& t, cudaStream_t s);
+const char* last_error();
+
+}  // namespace tc
+}  // namespace mel

@@ -1,0 +1,303 @@
+"""Thin ctypes binding of libmel (include/mel.h).  Argument marshalling only:
+every step of the method runs in the library's CUDA kernels.  There is no CPU
+fallback: if libmel.so is missing or fails to load this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmel.so")
+
+OK, EAGAIN, EOS = 0, 1, 2
+EINVAL, ECLOSED, EPROTO, ECUDA, ENCCL, ENOMEM, ENONFINITE = -1, -2, -3, -4, -5, -6, -7
+FP32, BF16 = 0, 1
+STORE_F32, STORE_BF16 = 0, 1
+FLAG_TIMING = 1
+K_COMMIT, K_SAMPLE, K_GATHER, K_HEAD_FWD, K_OUT_FWD_DW, K_OUT_DH, K_HEAD_BWD, K_ALLREDUCE, K_ADAM, K_LOSS = range(10)
+KERNEL_NAMES = ["commit", "sample", "gather", "head_fwd", "out_fwd_dw", "out_dh", "head_bwd", "allreduce",
+                "adam", "loss"]
+ABI_VERSION = 1
+
+EXPORTS = ["mel_config_default", "mel_nccl_unique_id", "mel_create", "mel_destroy", "mel_last_error",
+           "mel_param_layout", "mel_set_params", "mel_get_params", "mel_get_state", "mel_set_state",
+           "reservoir_put", "reservoir_close", "reservoir_sample_batch", "surrogate_step", "surrogate_eval",
+           "reservoir_stats", "reservoir_dump", "mel_sync", "mel_kernel_time", "mel_kernel_time_reset",
+           "mel_launch_count"]
+
+
+class MelError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__("libmel error %d: %s" % (code, msg))
+        self.code = code
+
+
+class _Config(C.Structure):
+    _fields_ = [("abi_version", C.c_uint32), ("n_field", C.c_uint32), ("hidden", C.c_uint32 * 2),
+                ("capacity", C.c_uint32), ("threshold", C.c_uint32), ("batch", C.c_uint32),
+                ("steps_per_sim", C.c_uint32), ("temp_lo", C.c_float), ("temp_hi", C.c_float),
+                ("precision", C.c_uint32), ("storage", C.c_uint32), ("lr0", C.c_double), ("lr_min", C.c_double),
+                ("lr_halving_samples", C.c_uint64), ("beta1", C.c_double), ("beta2", C.c_double),
+                ("eps", C.c_double), ("seed", C.c_uint64), ("staging_entries", C.c_uint32), ("flags", C.c_uint32)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("population", C.c_uint64), ("unseen", C.c_uint64), ("seen", C.c_uint64), ("puts", C.c_uint64),
+                ("committed", C.c_uint64), ("draws", C.c_uint64), ("evictions", C.c_uint64),
+                ("pending", C.c_uint64), ("steps", C.c_uint64), ("samples", C.c_uint64),
+                ("hist", C.c_uint64 * 64), ("over", C.c_uint32), ("closed", C.c_uint32), ("last_loss", C.c_double)]
+
+
+class _StateView(C.Structure):
+    _fields_ = [("p", C.POINTER(C.c_void_p)), ("m", C.POINTER(C.c_void_p)), ("v", C.POINTER(C.c_void_p)),
+                ("adam_step", C.c_uint64), ("samples_seen", C.c_uint64)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libmel.so (raises OSError if absent: no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise OSError("libmel.so not built at %s (run python -m paper_2309_16743_b200.build)" % path)
+    lib = C.CDLL(path)
+    vp, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int32
+    sig = {
+        "mel_config_default": (C.c_int, [C.POINTER(_Config), u32, u32]),
+        "mel_nccl_unique_id": (C.c_int, [vp]),
+        "mel_create": (C.c_int, [C.POINTER(_Config), C.c_int, C.c_int, vp, C.c_int, vp, C.POINTER(vp)]),
+        "mel_destroy": (None, [vp]),
+        "mel_last_error": (C.c_char_p, [vp]),
+        "mel_param_layout": (C.c_int, [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u64)]),
+        "mel_set_params": (C.c_int, [vp, C.POINTER(vp)]),
+        "mel_get_params": (C.c_int, [vp, C.POINTER(vp)]),
+        "mel_get_state": (C.c_int, [vp, C.POINTER(_StateView)]),
+        "mel_set_state": (C.c_int, [vp, C.POINTER(_StateView)]),
+        "reservoir_put": (C.c_int, [vp, u32, u32, C.POINTER(C.c_float), vp, C.c_int]),
+        "reservoir_close": (C.c_int, [vp]),
+        "reservoir_sample_batch": (C.c_int, [vp, C.POINTER(i32), C.POINTER(u32)]),
+        "surrogate_step": (C.c_int, [vp, C.POINTER(C.c_double)]),
+        "surrogate_eval": (C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(u32), C.POINTER(C.c_float), u32,
+                                     C.POINTER(C.c_double), C.POINTER(C.c_float)]),
+        "reservoir_stats": (C.c_int, [vp, C.POINTER(_Stats)]),
+        "reservoir_dump": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
+        "mel_sync": (C.c_int, [vp]),
+        "mel_kernel_time": (C.c_int, [vp, C.c_int, C.POINTER(C.c_double), C.POINTER(u64)]),
+        "mel_kernel_time_reset": (C.c_int, [vp]),
+        "mel_launch_count": (C.c_int, [vp, C.POINTER(u64)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+@dataclass
+class Config:
+    n_field: int
+    hidden: tuple = (256, 256)
+    capacity: int = 6000
+    threshold: int = 1000
+    batch: int = 10
+    steps_per_sim: int = 100
+    temp_lo: float = 100.0
+    temp_hi: float = 500.0
+    precision: int = FP32
+    storage: int = STORE_F32
+    lr0: float = 1e-3
+    lr_min: float = 2.5e-4
+    lr_halving_samples: int = 10000
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    seed: int = 1
+    staging_entries: int = 16
+    flags: int = 0
+
+    def to_c(self) -> _Config:
+        c = _Config()
+        c.abi_version = ABI_VERSION
+        c.n_field = self.n_field
+        h = list(self.hidden) + [0, 0]
+        c.hidden[0], c.hidden[1] = h[0], h[1]
+        for k in ("capacity", "threshold", "batch", "steps_per_sim", "temp_lo", "temp_hi", "precision", "storage",
+                  "lr0", "lr_min", "lr_halving_samples", "beta1", "beta2", "eps", "seed", "staging_entries", "flags"):
+            setattr(c, k, getattr(self, k))
+        return c
+
+
+def nccl_unique_id() -> bytes:
+    lib = load_library()
+    buf = C.create_string_buffer(128)
+    r = lib.mel_nccl_unique_id(buf)
+    if r != OK:
+        raise MelError(r, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+def _fptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+class Context:
+    """One rank's trainer + reservoir.  `device` is the CUDA ordinal; `stream` an
+    optional cudaStream_t handle (int)."""
+
+    def __init__(self, cfg: Config, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
+                 device: int = 0, stream: int | None = None):
+        self.lib = load_library()
+        self.cfg = cfg
+        self._c = cfg.to_c()
+        h = C.c_void_p()
+        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        r = self.lib.mel_create(C.byref(self._c), rank, world, idbuf, device, C.c_void_p(stream) if stream else None,
+                                C.byref(h))
+        if r != OK:
+            raise MelError(r, "mel_create failed (see stderr)")
+        self.h = h
+        n = C.c_uint32()
+        shapes = (C.c_uint32 * 12)()
+        tot = C.c_uint64()
+        self.lib.mel_param_layout(self.h, C.byref(n), shapes, C.byref(tot))
+        self.shapes = [(shapes[2 * i], shapes[2 * i + 1]) for i in range(n.value)]
+        self.n_params = tot.value
+
+    # -- lifecycle -------------------------------------------------------------------
+    def close_ctx(self):
+        if getattr(self, "h", None):
+            self.lib.mel_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close_ctx()
+        except Exception:
+            pass
+
+    def _check(self, r, allowed=(OK,)):
+        if r in allowed:
+            return r
+        msg = self.lib.mel_last_error(self.h).decode(errors="replace") if self.h else ""
+        raise MelError(r, msg)
+
+    # -- reservoir ---------------------------------------------------------------------
+    def put(self, sim: int, t: int, X, field) -> int:
+        Xa = np.ascontiguousarray(X, dtype=np.float32)
+        if hasattr(field, "data_ptr"):                       # torch tensor
+            on_dev = 1 if field.is_cuda else 0
+            ptr = C.c_void_p(field.data_ptr())
+        else:
+            field = np.ascontiguousarray(field, dtype=np.float32)
+            on_dev, ptr = 0, field.ctypes.data_as(C.c_void_p)
+        return self._check(self.lib.reservoir_put(self.h, sim, t, _fptr(Xa), ptr, on_dev), (OK, EAGAIN))
+
+    def close(self) -> int:
+        return self._check(self.lib.reservoir_close(self.h))
+
+    def sample(self, want_slots: bool = False, want_n: bool = False):
+        """Returns (status, slots or None, n or None)."""
+        slots = np.zeros(self.cfg.batch, dtype=np.int32) if want_slots else None
+        n = C.c_uint32()
+        r = self.lib.reservoir_sample_batch(self.h, slots.ctypes.data_as(C.POINTER(C.c_int32)) if want_slots else None,
+                                            C.byref(n) if (want_slots or want_n) else None)
+        self._check(r, (OK, EAGAIN))
+        nn = n.value if (want_slots or want_n) else None
+        return r, (slots[:nn] if want_slots else None), nn
+
+    def step(self, want_loss: bool = True):
+        loss = C.c_double()
+        r = self.lib.surrogate_step(self.h, C.byref(loss) if want_loss else None)
+        self._check(r, (OK, EAGAIN, EOS))
+        return r, (loss.value if (want_loss and r == OK) else None)
+
+    def eval(self, X, t, fields=None, want_pred=False):
+        X = np.ascontiguousarray(X, dtype=np.float32)
+        t = np.ascontiguousarray(t, dtype=np.uint32)
+        n = X.shape[0]
+        f = np.ascontiguousarray(fields, dtype=np.float32) if fields is not None else None
+        pred = np.zeros((n, self.cfg.n_field), dtype=np.float32) if want_pred else None
+        mse = C.c_double()
+        self._check(self.lib.surrogate_eval(self.h, _fptr(X), t.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                            _fptr(f) if f is not None else None, n, C.byref(mse),
+                                            _fptr(pred) if want_pred else None))
+        return mse.value, pred
+
+    def stats(self) -> dict:
+        s = _Stats()
+        self._check(self.lib.reservoir_stats(self.h, C.byref(s)))
+        d = {k: getattr(s, k) for k, _ in _Stats._fields_ if k != "hist"}
+        d["hist"] = np.array(list(s.hist), dtype=np.int64)
+        return d
+
+    def dump(self, payload: bool = True) -> dict:
+        Cn, N = self.cfg.capacity, self.cfg.n_field
+        sim = np.zeros(Cn, np.uint32); t = np.zeros(Cn, np.uint32); X = np.zeros((Cn, 5), np.float32)
+        seen = np.zeros(Cn, np.uint32); ps = np.zeros(Cn, np.uint64)
+        pl = None
+        if payload:
+            pl = np.zeros((Cn, N), np.float32 if self.cfg.storage == STORE_F32 else np.uint16)
+        v = lambda a: a.ctypes.data_as(C.c_void_p)
+        self._check(self.lib.reservoir_dump(self.h, v(sim), v(t), v(X), v(seen), v(ps), v(pl) if payload else None))
+        return dict(sim=sim, t=t, X=X, seen=seen, put_seq=ps, payload=pl)
+
+    # -- parameters / state ------------------------------------------------------------
+    def _arrays(self):
+        return [np.zeros(s, dtype=np.float32) if s[1] != 1 else np.zeros(s[0], dtype=np.float32)
+                for s in self.shapes]
+
+    @staticmethod
+    def _ptrs(arrs):
+        return (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+
+    def get_params(self):
+        out = self._arrays()
+        self._check(self.lib.mel_get_params(self.h, self._ptrs(out)))
+        return out
+
+    def set_params(self, tensors):
+        arrs = [np.ascontiguousarray(t, dtype=np.float32) for t in tensors]
+        self._check(self.lib.mel_set_params(self.h, self._ptrs(arrs)))
+
+    def get_state(self):
+        p, m, v = self._arrays(), self._arrays(), self._arrays()
+        sv = _StateView()
+        pp, mp, vp = self._ptrs(p), self._ptrs(m), self._ptrs(v)
+        sv.p, sv.m, sv.v = C.cast(pp, C.POINTER(C.c_void_p)), C.cast(mp, C.POINTER(C.c_void_p)), C.cast(vp, C.POINTER(C.c_void_p))
+        self._check(self.lib.mel_get_state(self.h, C.byref(sv)))
+        return dict(p=p, m=m, v=v, k=sv.adam_step, S=sv.samples_seen)
+
+    def set_state(self, st):
+        p = [np.ascontiguousarray(x, np.float32) for x in st["p"]]
+        m = [np.ascontiguousarray(x, np.float32) for x in st["m"]]
+        v = [np.ascontiguousarray(x, np.float32) for x in st["v"]]
+        sv = _StateView()
+        pp, mp, vp = self._ptrs(p), self._ptrs(m), self._ptrs(v)
+        sv.p, sv.m, sv.v = C.cast(pp, C.POINTER(C.c_void_p)), C.cast(mp, C.POINTER(C.c_void_p)), C.cast(vp, C.POINTER(C.c_void_p))
+        sv.adam_step, sv.samples_seen = st["k"], st["S"]
+        self._check(self.lib.mel_set_state(self.h, C.byref(sv)))
+
+    # -- misc ---------------------------------------------------------------------------
+    def sync(self):
+        self._check(self.lib.mel_sync(self.h))
+
+    def kernel_time(self, k: int):
+        ms, n = C.c_double(), C.c_uint64()
+        self._check(self.lib.mel_kernel_time(self.h, k, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def kernel_time_reset(self):
+        self._check(self.lib.mel_kernel_time_reset(self.h))
+
+    def launch_count(self) -> int:
+        n = C.c_uint64()
+        self._check(self.lib.mel_launch_count(self.h, C.byref(n)))
+        return n.value

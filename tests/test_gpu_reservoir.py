@@ -1,0 +1,125 @@
+"""GPU parity of the reservoir path (Alg. 1) and of the fp32 training
+step, through the C ABI, against the oracle on the same seeded op-logs.
+Bar: reservoir contents, sampled slots and counters bit-exact; fp32-mode loss and
+per-tensor weights within 1e-5 relative (re-anchored, BASELINE north_star)."""
+import random
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+from mel_inputs import design
+from oracle import mlp, reservoir as ores
+
+from harness import FieldTable, compare_reservoir, make_config, replay_parity
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mel():
+    from paper_2309_16743_b200 import build, mel as m
+    build.build()
+    return m
+
+
+@pytest.mark.parametrize("wl", [design.TINY, design.MEDIUM], ids=["tiny", "medium"])
+def test_init_params_bit_exact(mel, wl):
+    ctx = mel.Context(make_config(replace(wl, capacity=512, threshold=100)))
+    got = ctx.get_params()
+    want = [x for Wb in mlp.init_params(mlp.layer_dims(wl.n_field, wl.hidden), seed=1) for x in Wb]
+    for g, w in zip(got, want):
+        assert np.array_equal(g.reshape(-1).view(np.uint32), w.reshape(-1).view(np.uint32))
+
+
+@pytest.mark.parametrize("wl,storage", [(design.TINY, 0), (design.TINY_EVICT, 0), (design.TINY_EVICT, 1)],
+                         ids=["tiny-f32", "tiny_evict-f32", "tiny_evict-bf16store"])
+def test_tiny_oplog_to_eos_reanchored(mel, wl, storage):
+    table = FieldTable(wl)
+    ctx = mel.Context(make_config(wl, storage=storage))
+    rep = replay_parity(ctx, wl, table, design.build_oplog(wl), storage=storage)
+    res = rep["oracle_res"]
+    assert res.over and res.p == 0, "replay must reach EOS"
+    compare_reservoir(ctx, res, storage)
+    assert rep["steps"] > 20
+    assert max(rep["loss_err"]) <= 1e-5, max(rep["loss_err"])
+    assert max(rep["w_err"]) <= 1e-5, max(rep["w_err"])
+    if wl.capacity < wl.sims * wl.tau:
+        assert res.evictions > 0
+
+
+def test_medium_geometry_with_evictions_reanchored(mel):
+    wl = replace(design.MEDIUM, name="medium-evict", capacity=2000, threshold=333, sims=60)
+    table = FieldTable(wl)
+    ctx = mel.Context(make_config(wl))
+    ops = design.build_oplog(wl)
+    rep = replay_parity(ctx, wl, table, ops, max_train_steps=25)
+    compare_reservoir(ctx, rep["oracle_res"])
+    assert rep["oracle_res"].evictions > 0
+    assert max(rep["loss_err"]) <= 1e-5 and max(rep["w_err"]) <= 1e-5, (max(rep["loss_err"]), max(rep["w_err"]))
+
+
+@pytest.mark.parametrize("seed", [3, 4])
+def test_random_schedules_with_backpressure_and_ring_wrap(mel, seed):
+    """Random interleavings (bursty producer, small C so that u == C back-pressure
+    happens, staging ring of 6 entries so reservoir_put returns EAGAIN), no
+    training: slots and final contents bit-exact."""
+    wl = replace(design.TINY, capacity=8, threshold=2, batch=2)
+    table = FieldTable(wl)
+    ctx = mel.Context(make_config(wl, staging=6, seed=seed))
+    res = ores.Reservoir(wl.capacity, wl.threshold, wl.n_field, seed=seed)
+    rng = random.Random(seed)
+    order = design.stream_order(wl.sims, wl.tau)
+    i = 0
+    backpressure = ring_full = 0
+    while i < len(order):
+        for _ in range(rng.randrange(14)):
+            if i >= len(order):
+                break
+            s, t = order[i]
+            r = ctx.put(s, t, table.Xs(s), table.field(s, t))
+            if r == 1:
+                ring_full += 1
+                break
+            res.put(s, t, table.Xs(s), table.field(s, t))
+            i += 1
+        st_o, sl_o = res.sample(wl.batch)
+        st_g, sl_g, n = ctx.sample(want_slots=True)
+        assert st_o == st_g and list(sl_g) == list(sl_o)
+        backpressure += int(len(res.pend) > 0)
+        ctx.step(want_loss=False) if st_g == 0 else None
+    ctx.close(); res.close()
+    while True:
+        st_o, sl_o = res.sample(wl.batch)
+        st_g, sl_g, n = ctx.sample(want_slots=True)
+        assert list(sl_g) == list(sl_o)
+        if not sl_o:
+            break
+    compare_reservoir(ctx, res)
+    assert backpressure > 0 and ring_full > 0
+    with pytest.raises(mel.MelError) as e:
+        ctx.put(0, 0, table.Xs(0), table.field(0, 0))
+    assert e.value.code == mel.ECLOSED
+    with pytest.raises(mel.MelError) as e:
+        ctx.close()
+    assert e.value.code == mel.EPROTO
+
+
+def test_device_resident_puts_match_host_puts(mel):
+    import torch
+    wl = design.TINY_EVICT
+    table = FieldTable(wl)
+    a = mel.Context(make_config(wl))
+    b = mel.Context(make_config(wl))
+    keep = []    # device sources must stay alive until the library's stream read them
+    for (s, t) in design.stream_order(wl.sims, wl.tau)[:60]:
+        f = table.field(s, t)
+        a.put(s, t, table.Xs(s), f)
+        keep.append(torch.from_numpy(f).cuda())
+        torch.cuda.synchronize()
+        b.put(s, t, table.Xs(s), keep[-1])
+        if t % 5 == 4:
+            assert list(a.sample(True)[1]) == list(b.sample(True)[1])
+    da, db = a.dump(), b.dump()
+    for k in da:
+        assert np.array_equal(da[k], db[k]), k

@@ -1,0 +1,93 @@
+"""GPU parity of the training step in bf16 mode (tcgen05 output layer) and of
+validation, against the oracle.  Tolerances: DESIGN.md "Parity bars"."""
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+from mel_inputs import design
+from oracle import mlp, reservoir as ores, trainer as otr
+
+from harness import FieldTable, make_config, rel_norm, replay_parity, tensors_f64
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mel():
+    from paper_2309_16743_b200 import build, mel as m
+    build.build()
+    return m
+
+
+def _bf16_wl(**kw):
+    base = replace(design.MEDIUM, name="medium-bf16", capacity=2000, threshold=333, sims=60)
+    return replace(base, **kw)
+
+
+@pytest.mark.parametrize("n,batch", [(100, 256), (37, 64), (101, 192)], ids=["N1e4-B256", "N1369-B64", "N10201-B192"])
+def test_bf16_step_reanchored(mel, n, batch):
+    """One re-anchored bf16 step at a time: the GPU's output layer runs on
+    tcgen05 with bf16 operands (W shadow, H, dY) and fp32 TMEM accumulation.
+    Sizes span several 128-row tiles, ragged tails (N % 128 != 0) and B not a
+    multiple of 128."""
+    wl = _bf16_wl(n=n, batch=batch, hidden=(256, 256))
+    table = FieldTable(wl)
+    ctx = mel.Context(make_config(wl, precision=1, storage=1))
+    rep = replay_parity(ctx, wl, table, design.build_oplog(wl), storage=1, max_train_steps=6)
+    print("bf16 re-anchored: loss err %.3e  weight err %.3e" % (max(rep["loss_err"]), max(rep["w_err"])))
+    assert rep["steps"] == 6
+    assert max(rep["loss_err"]) <= 2e-2
+    assert max(rep["w_err"]) <= 1e-3
+
+
+@pytest.mark.slow
+def test_bf16_loss_after_1000_steps_free_running(mel):
+    """north_star: <= 2e-2 relative loss at step 1000 in bf16 mode (same batches,
+    free-running from the same init)."""
+    wl = replace(design.MEDIUM, name="medium-1k", capacity=6000, threshold=1000, sims=1100, puts_per_step=100)
+    table = FieldTable(wl)
+    ctx = mel.Context(make_config(wl, precision=1, storage=1))
+    tr = otr.Trainer(wl.n_field, wl.hidden, wl.tau, wl.capacity, wl.threshold, wl.batch, seed=1, storage=1)
+    losses_g, losses_o = [], []
+    for op in design.build_oplog(wl):
+        if op[0] == "PUT":
+            _, r, s, t = op
+            ctx.put(s, t, table.Xs(s), table.field(s, t)); tr.put(0, s, t, table.Xs(s), table.field(s, t))
+        elif op[0] == "SAMPLE":
+            a = ctx.sample()[0]; b = tr.sample(0)[0]
+            assert a == b
+        elif op[0] == "STEP":
+            a, lg = ctx.step(want_loss=True)
+            b, lo = tr.step()
+            assert a == b
+            if a == 0:
+                losses_g.append(lg); losses_o.append(lo)
+                if len(losses_g) == 1000:
+                    break
+    assert len(losses_g) == 1000
+    err = abs(losses_g[-1] - losses_o[-1]) / losses_o[-1]
+    tail = np.mean(np.abs(np.array(losses_g[-50:]) - np.array(losses_o[-50:])) / np.array(losses_o[-50:]))
+    print("bf16 step-1000 loss rel err %.3e (mean over 951-1000: %.3e); loss %.4e -> %.4e" %
+          (err, tail, losses_o[0], losses_o[-1]))
+    assert err <= 2e-2
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_eval_matches_oracle(mel, precision):
+    wl = _bf16_wl(n=40, batch=128)
+    table = FieldTable(wl)
+    ctx = mel.Context(make_config(wl, precision=precision, storage=precision))
+    Xv = design.draw_design(3, seed=1, validation=True)
+    from mel_inputs import heat
+    fields = np.concatenate([heat.simulate(Xv[i], wl.n, wl.tau) for i in range(3)])
+    X = np.repeat(Xv, wl.tau, axis=0)
+    t = np.tile(np.arange(wl.tau), 3).astype(np.uint32)
+    mse, pred = ctx.eval(X, t, fields, want_pred=True)
+    params = [(W.astype(np.float64), b.astype(np.float64)) for W, b in mlp.unflatten(ctx.get_params())]
+    xn = mlp.normalise_inputs(X, t, wl.tau)
+    tn = ores.normalise_f32(fields).astype(np.float64)
+    want = mlp.mse(params, xn, tn)
+    assert abs(mse - want) / want < 1e-5
+    Y = mlp.forward(params, xn)[1][-1] * 400.0 + 100.0
+    assert np.max(np.abs(pred - Y)) < 1e-2
