@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""bench.py -- reservoir-fed online training of the paper-shaped heat-equation
+MLP surrogate (arXiv 2309.16743; BASELINE.json configs[2], and configs[3] per
+rank under torchrun) on B200.
+
+One timed step = the whole hot path of SURVEY §8(a) for one batch per rank:
+k device-resident reservoir_put calls (the streamed clients' time steps), one
+reservoir_sample_batch (commit with eviction, watermark gate, Philox sampling),
+one surrogate_step (gather, head fwd, tcgen05 output layer fwd+MSE+dW, split-K
+dH, head bwd, NCCL gradient all-reduce when N > 1, Adam + LR schedule).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "surrogate training samples/sec at 1/2/4/8 B200; % tensor-core roofline; val MSE"
+UNIT = "samples/s"
+N_GRID, TAU, SIMS = 1000, 100, 10000
+HIDDEN = (256, 256)
+CAP, THETA, BATCH = 6000, 1000, 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--puts-per-step", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--grid", type=int, default=N_GRID)
+    ap.add_argument("--batch", type=int, default=BATCH)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "fallback": True}
+
+
+def config_block(args, world):
+    return {"workload": "paper-shaped (BASELINE configs[%d])" % (2 if world == 1 else 3),
+            "field": "%dx%d" % (args.grid, args.grid), "tau": TAU, "sims_streamed": SIMS,
+            "mlp": "6-256-256-%d" % (args.grid * args.grid), "capacity": CAP, "threshold": THETA,
+            "batch_per_rank": args.batch, "global_batch": args.batch * world, "puts_per_step": args.puts_per_step,
+            "routing": "(sim + t) mod R", "precision": "bf16 tcgen05 output layer, fp32 master/Adam",
+            "target_storage": "bf16", "l2": "inputs larger than L2 (W 0.5 GB, Adam state 3 GB, targets 2 GB / step)",
+            "parallelism": "dp%d" % world}
+
+
+# ------------------------------------------------------------------------------------
+# oracle timing (cpu_baseline and --impl reference): the oracle as it stands
+# ------------------------------------------------------------------------------------
+def oracle_rate(budget_s: float, batch: int, n_full: int, phi_host=None, grid=N_GRID):
+    """Time oracle training steps (sample from an oracle reservoir + fp64
+    forward/backward + Adam) on the B-row batch at two output widths and
+    extrapolate linearly in the output width to the paper's N (the output layer is
+    99.97% of the work and linear in N).  Returns (samples_per_s, sample_desc, threads)."""
+    import numpy as np
+    from mel_inputs import design
+    from oracle import trainer as otr
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        threads = 1
+    X = design.draw_design(64, seed=1)
+    rng = np.random.default_rng(0)
+
+    def run(width, max_steps, t_budget):
+        tr = otr.Trainer(width, HIDDEN, TAU, CAP, THETA, batch, seed=1, storage=1)
+        # fill past the watermark with heat-like fields (a width-`width` sample of the real rows)
+        for i in range(THETA + 1):
+            s, t = i % 64, (i // 64) % TAU
+            f = (100.0 + 400.0 * rng.random(width)).astype(np.float32) if phi_host is None else \
+                (X[s] @ phi_host[:, t, :width]).astype(np.float32)
+            tr.put(0, s, t, X[s], f)
+        tr.sample(0); tr.step()                      # warm-up step
+        n, t0 = 0, time.perf_counter()
+        while n < max_steps and (time.perf_counter() - t0) < t_budget:
+            tr.sample(0); tr.step()
+            n += 1
+        return (time.perf_counter() - t0) / max(n, 1), n
+
+    w1, w2 = 1024, 4096
+    t1, n1 = run(w1, 50, budget_s * 0.3)
+    t2, n2 = run(w2, 50, budget_s * 0.7)
+    slope = max(t2 - t1, 0.0) / (w2 - w1)
+    t_full = t1 + slope * (n_full - w1)
+    desc = ("%d+%d oracle steps (fp64 numpy) at B=%d on the 6-256-256-N model with N=%d and N=%d output columns, "
+            "linearly extrapolated in N to N=%d" % (n1, n2, batch, w1, w2, n_full))
+    return batch / t_full, desc, threads, t_full
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    cores = len(os.sched_getaffinity(0))
+    n_full = args.grid * args.grid
+    # each reference "step" is one extrapolated oracle step; bound the whole run to a few minutes
+    budget = min(120.0, 8.0 * (args.steps + args.warmup))
+    rate, desc, threads, t_full = oracle_rate(budget, args.batch, n_full)
+    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(args, world),
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "host_cores": cores, "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------
+class Clocks:
+    def __init__(self, idx):
+        self.idx, self.p, self.path = idx, None, "/tmp/mel_clocks_%d.csv" % os.getpid()
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + q, "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+            self.f.close()
+
+    def summary(self):
+        try:
+            rows = [l.split(",") for l in open(self.path).read().strip().splitlines()]
+            sm = [float(r[1]) for r in rows if len(r) >= 9]
+            mx = max(float(r[2]) for r in rows if len(r) >= 9)
+            reasons = set()
+            for r in rows:
+                for name, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"], r[5:9]):
+                    if v.strip() == "Active":
+                        reasons.add(name)
+            loaded = [s for s in sm if s > 0.5 * mx] or sm
+            return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                    "samples": len(sm)}
+        except Exception as e:
+            return {"error": str(e)}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from mel_inputs import design, heat_torch
+    from paper_2309_16743_b200 import mel
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    nccl_id = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [mel.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    n_field = args.grid * args.grid
+    B, k = args.batch, args.puts_per_step
+    cfg = mel.Config(n_field=n_field, hidden=HIDDEN, capacity=CAP, threshold=THETA, batch=B, steps_per_sim=TAU,
+                     precision=mel.BF16, storage=mel.STORE_BF16, seed=1, staging_entries=32)
+    stream = torch.cuda.current_stream(dev)
+    ctx = mel.Context(cfg, rank=rank, world=world, nccl_id=nccl_id, device=local, stream=stream.cuda_stream)
+
+    # synthetic ensemble: exact heat solutions by linearity from a GPU-generated basis
+    phi = heat_torch.basis(args.grid, TAU, device=dev)                       # (5, tau, N) fp32
+    Xd = torch.from_numpy(design.draw_design(SIMS, seed=1)).to(dev)
+    order = [(s, t) for s in range(SIMS) for t in range(TAU) if (s + t) % world == rank]
+    cursor = [0]
+
+    def next_batch(n):
+        pairs = order[cursor[0]:cursor[0] + n]
+        cursor[0] += n
+        s = torch.tensor([p[0] for p in pairs], device=dev)
+        t = torch.tensor([p[1] for p in pairs], device=dev)
+        return pairs, Xd[s], heat_torch.fields(phi, Xd[s], t)
+
+    def put_many(pairs, Xs, F):
+        Xh = Xs.cpu().numpy()
+        for i, (s, t) in enumerate(pairs):
+            r = ctx.put(s, t, Xh[i], F[i])
+            assert r == 0, "staging ring full"
+
+    # warm-up phase 1: stream until the reservoir is full (P:321 C = 6000)
+    filled = 0
+    while filled < CAP:
+        pairs, Xs, F = next_batch(16)
+        put_many(pairs, Xs, F)
+        filled += len(pairs)
+        st, _, _ = ctx.sample()
+        ctx.step(want_loss=False)
+        torch.cuda.current_stream(dev).synchronize()
+    # device-resident pool of the timed steps' streamed fields
+    total_steps = args.warmup + args.steps
+    pool = [next_batch(k) for _ in range(total_steps + 12)]
+    torch.cuda.synchronize()
+
+    def one_step(i, want_loss=False):
+        pairs, Xs, F = pool[i]
+        Xh = pool_X[i]
+        for j, (s, t) in enumerate(pairs):
+            ctx.put(s, t, Xh[j], F[j])
+        ctx.sample()
+        return ctx.step(want_loss=want_loss)
+
+    pool_X = [p[1].cpu().numpy() for p in pool]
+    for i in range(args.warmup):
+        one_step(i)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        tt = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return tt.item()
+
+    # ---- timed region (device-resident inputs) ----
+    barrier()
+    torch.cuda.synchronize()
+    l0 = ctx.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for i in range(args.warmup, total_steps):
+            one_step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = ctx.launch_count() - l0
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    ms_step = ms / args.steps
+    value = B * world * args.steps / (ms / 1e3)
+
+    # ---- per-kernel timing pass (CUDA events around each kernel class) ----
+    ctx.set_flags(mel.FLAG_TIMING)
+    ctx.kernel_time_reset()
+    n_kt = min(args.steps, 10)
+    extra = [next_batch(k) for _ in range(n_kt)]
+    extra_X = [e[1].cpu().numpy() for e in extra]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(n_kt):
+        pairs, Xs, F = extra[i]
+        for j, (s, t) in enumerate(pairs):
+            ctx.put(s, t, extra_X[i][j], F[j])
+        ctx.sample()
+        ctx.step(want_loss=False)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    kt_total = e0.elapsed_time(e1)
+    kernels = {}
+    for kid, name in enumerate(mel.KERNEL_NAMES):
+        tms, nl = ctx.kernel_time(kid)
+        kernels[name] = {"ms_per_step": tms / n_kt, "share": tms / kt_total if kt_total else None}
+    ctx.set_flags(0)
+    P = peaks()
+    K = HIDDEN[-1]
+    n_params = ctx.n_params
+    alg = {
+        "out_fwd_dw": ("tensor", 4.0 * B * n_field * K),                    # Y = H W^T and dW = dY^T H
+        "out_dh": ("tensor", 2.0 * B * n_field * K),                        # dH = dY W
+        "adam": ("hbm", 28.0 * n_params + 2.0 * n_field * K),               # p,m,v,g in; p,m,v out; bf16 W shadow
+    }
+    dom = max(alg, key=lambda n: kernels[n]["ms_per_step"])
+    bound, work = alg[dom]
+    dur_s = kernels[dom]["ms_per_step"] / 1e3
+    if bound == "tensor":
+        peak, unit_r = P.get("bf16_tflops_sustained", P.get("bf16_tflops")), "TFLOP/s"
+        achieved = work / dur_s / 1e12
+    else:
+        peak, unit_r = P["hbm_gbs"], "GB/s"
+        achieved = work / dur_s / 1e9
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = prof.get(dom, {}).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {"kernel": dom, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit_r,
+                "frac": achieved / peak, "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json %s" % ("bf16_tflops_sustained" if bound == "tensor" else "hbm_gbs")}
+    for name, (b_, w_) in alg.items():
+        d = kernels[name]["ms_per_step"] / 1e3
+        if d > 0:
+            kernels[name]["achieved"] = w_ / d / (1e12 if b_ == "tensor" else 1e9)
+            kernels[name]["unit"] = "TFLOP/s" if b_ == "tensor" else "GB/s"
+    step_flops = (6.0 * B * n_field * K + 6.0 * B * K * K + 4.0 * B * 6 * K)
+    tensor_frac_step = step_flops / (ms_step / 1e3) / 1e12 / P["bf16_tflops"]
+
+    # ---- end-to-end through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        n_e2e = min(args.steps, 20)
+        host = [next_batch(k) for _ in range(n_e2e)]
+        host = [(p, Xs.cpu().numpy(), F.cpu().pin_memory()) for p, Xs, F in host]
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        for pairs, Xh, Fh in host:
+            for j, (s, t) in enumerate(pairs):
+                ctx.put(s, t, Xh[j], Fh[j])          # pinned host -> device (copy stream)
+            ctx.sample()
+            ctx.step(want_loss=True)                 # device -> host loss read every step
+        torch.cuda.synchronize()
+        wall = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": B * world * n_e2e / wall, "unit": UNIT, "h2d_bytes_per_step": k * (4 * n_field + 32),
+               "d2h_bytes_per_step": 8, "steps": n_e2e, "timing": "host wall clock, max over ranks"}
+
+    # ---- validation MSE on one held-out simulation ----
+    val = None
+    try:
+        Xv = torch.from_numpy(design.draw_design(1, seed=1, validation=True)).to(dev)
+        tv = torch.arange(TAU, device=dev)
+        Fv = heat_torch.fields(phi, Xv.repeat(TAU, 1), tv).cpu().numpy()
+        mse, _ = ctx.eval(Xv.repeat(TAU, 1).cpu().numpy(), tv.cpu().numpy().astype(np.uint32), Fv)
+        val = {"mse_normalised": mse, "mse_K2": mse * 400.0 ** 2, "samples": TAU}
+    except Exception as e:
+        val = {"error": str(e)}
+    stats = ctx.stats()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        phi_h = phi[:, :, :4096].double().cpu().numpy()
+        rate, desc, threads, _ = oracle_rate(20.0, B, n_field, phi_host=phi_h)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "host_cores": len(os.sched_getaffinity(0)),
+               "kind": "oracle", "sample": desc}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (exact heat-equation solutions, seeded)",
+            "config": config_block(args, world), "gpu_launches": launches, "clocks": clk.summary(),
+            "roofline": roofline, "tensor_frac_step": tensor_frac_step, "kernels": kernels,
+            "cpu_baseline": cpu, "e2e": e2e, "val_mse": val,
+            "reservoir": {"population": stats["population"], "unseen": stats["unseen"],
+                          "evictions": stats["evictions"], "puts": stats["puts"], "draws": stats["draws"],
+                          "repeats_per_unique": stats["draws"] / max(1, stats["committed"])}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close_ctx()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

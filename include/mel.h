@@ -220,6 +220,8 @@ enum mel_kernel {
 };
 int mel_kernel_time(mel_ctx* ctx, int k, double* ms_host, uint64_t* launches_host);
 int mel_kernel_time_reset(mel_ctx* ctx);
+/* Replaces cfg.flags (MEL_FLAG_*) from the next call on.  Always MEL_OK. */
+int mel_set_flags(mel_ctx* ctx, uint32_t flags);
 /* Number of library kernel launches since creation (bench "gpu_launches"). */
 int mel_launch_count(const mel_ctx* ctx, uint64_t* n_host);
 

@@ -890,6 +890,12 @@ int mel_kernel_time_reset(mel_ctx* c) {
   return MEL_OK;
 }
 
+int mel_set_flags(mel_ctx* c, uint32_t flags) {
+  GUARD(c);
+  c->cfg.flags = flags;
+  return MEL_OK;
+}
+
 int mel_launch_count(const mel_ctx* c, uint64_t* n) {
   if (!c || !n) return MEL_EINVAL;
   *n = c->launches;

@@ -88,3 +88,11 @@ def test_t0_emits_initial_condition_everywhere_and_tau_steps():
     g = f[1].reshape(6, 6)
     assert np.all(g[1:-1, 0] == 100) and np.all(g[1:-1, -1] == 300)
     assert np.all(g[0, 1:-1] == 200) and np.all(g[-1, 1:-1] == 400)
+
+
+def test_torch_generator_matches_numpy_generator():
+    import torch
+    from mel_inputs import heat_torch
+    phi_t = heat_torch.basis(9, 5, device="cpu", out_dtype=torch.float64).numpy()
+    phi_n = heat.basis(9, 5)
+    np.testing.assert_allclose(phi_t, phi_n, rtol=1e-11, atol=1e-12)
