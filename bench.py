@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--grid", type=int, default=N_GRID)
     ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--profile", action="store_true", help="timed region only (for ncu)")
     return ap.parse_args()
 
 
@@ -197,7 +198,10 @@ def main():
     B, k = args.batch, args.puts_per_step
     cfg = mel.Config(n_field=n_field, hidden=HIDDEN, capacity=CAP, threshold=THETA, batch=B, steps_per_sim=TAU,
                      precision=mel.BF16, storage=mel.STORE_BF16, seed=1, staging_entries=32)
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated stream shared by torch (events, data generation) and libmel, so
+    # that CUDA events bracket exactly the library's work
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     ctx = mel.Context(cfg, rank=rank, world=world, nccl_id=nccl_id, device=local, stream=stream.cuda_stream)
 
     # synthetic ensemble: exact heat solutions by linearity from a GPU-generated basis
@@ -263,10 +267,12 @@ def main():
     l0 = ctx.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
+        torch.cuda.nvtx.range_push("timed")
         ev0.record(stream)
         for i in range(args.warmup, total_steps):
             one_step(i)
         ev1.record(stream)
+        torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
     barrier()
     launches = ctx.launch_count() - l0
@@ -274,6 +280,10 @@ def main():
     ms_step = ms / args.steps
     value = B * world * args.steps / (ms / 1e3)
 
+    if args.profile:
+        if rank == 0:
+            print(json.dumps({"ms_per_step": ms_step, "value": value}), flush=True)
+        return 0
     # ---- per-kernel timing pass (CUDA events around each kernel class) ----
     ctx.set_flags(mel.FLAG_TIMING)
     ctx.kernel_time_reset()

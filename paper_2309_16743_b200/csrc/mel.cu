@@ -248,10 +248,18 @@ int world_allreduce(mel_ctx* c) {
   return MEL_OK;
 }
 
+int head_splits(uint32_t B, uint64_t out_elems, size_t part_elems) {
+  int sk = (int)(B / 128);
+  if (sk > 16) sk = 16;
+  while (sk > 1 && (size_t)sk * out_elems > part_elems) --sk;
+  return sk < 1 ? 1 : sk;
+}
+
 // backward of the head layers given dZ of the last hidden layer (d_dz[L-2])
 int head_backward(mel_ctx* c) {
   const int L = c->L;
-  Timer t(c, MEL_K_HEAD_BWD, 3 * (L - 1));
+  Timer t(c, MEL_K_HEAD_BWD, 0);
+  uint64_t nl = 0;
   for (int l = L - 1; l >= 1; --l) {             // weight layer l (1-based), l < L
     const int dout = c->dims[l], din = c->dims[l - 1];
     const float* dZ = c->d_dz[l - 1];
@@ -259,15 +267,29 @@ int head_backward(mel_ctx* c) {
     const int ldin = (l == 1) ? 8 : din;
     float* gW = c->d_g + c->off[2 * (l - 1)];
     float* gb = c->d_g + c->off[2 * (l - 1) + 1];
-    sgemm(true, false, dout, din, (int)c->B, dZ, dout, Hin, ldin, gW, din, EPI_STORE, nullptr, nullptr, 0, 1, c->stream);
+    // dW = dZ^T H_in reduces over the batch: split-K so the tiny output grid fills the SMs
+    const int sk = head_splits(c->B, (uint64_t)dout * din, c->part_elems);
+    if (sk > 1) {
+      sgemm(true, false, dout, din, (int)c->B, dZ, dout, Hin, ldin, c->d_part, din, EPI_STORE, nullptr, nullptr, 0,
+            sk, c->stream);
+      splitk_reduce(dout, din, sk, c->d_part, gW, din, nullptr, 0, c->stream);
+      ++nl;
+    } else {
+      sgemm(true, false, dout, din, (int)c->B, dZ, dout, Hin, ldin, gW, din, EPI_STORE, nullptr, nullptr, 0, 1,
+            c->stream);
+    }
     col_sum(dZ, (int)c->B, dout, dout, gb, c->stream);
+    nl += 2;
     if (l > 1) {
+      nl += 2;
       const float* W = c->d_p + c->off[2 * (l - 1)];
       sgemm(false, false, (int)c->B, din, dout, dZ, dout, W, din, c->d_dz[l - 2], din, EPI_STORE, nullptr, nullptr, 0, 1,
             c->stream);
       relu_mask_mul(c->d_dz[l - 2], c->d_z[l - 2], (uint64_t)c->B * din, c->stream);
     }
   }
+  c->launches += nl;
+  c->klaunch[MEL_K_HEAD_BWD] += nl;
   return check_launch(c, "head backward");
 }
 
@@ -477,6 +499,7 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
     DALLOC(c->d_dy, (size_t)c->B * c->Npad);
     const int sp = splits_for(c->Npad);
     c->part_elems = (size_t)sp * c->B * c->Klast;
+    if (c->part_elems < (size_t)16 * c->hmax * c->hmax) c->part_elems = (size_t)16 * c->hmax * c->hmax;
     DALLOC(c->d_part, c->part_elems);
     c->max_parts = (int)(((c->Npad + 63) / 64) * ((c->B + 63) / 64));
     DALLOC(c->d_sse_part, c->max_parts);
@@ -485,6 +508,7 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
     r = tc::alloc_buffers(c->tcb, c->Npad, c->B, c->Klast);
     if (r) return fail(c, MEL_ENOMEM, "tensor-core scratch allocation failed");
     c->part_elems = tc::dh_part_elems(c->B, c->Klast);
+    if (c->part_elems < (size_t)16 * c->hmax * c->hmax) c->part_elems = (size_t)16 * c->hmax * c->hmax;
     DALLOC(c->d_part, c->part_elems);
     c->max_parts = tc::max_sse_parts(c->Npad);
     DALLOC(c->d_sse_part, c->max_parts);

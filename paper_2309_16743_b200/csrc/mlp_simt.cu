@@ -209,38 +209,57 @@ __global__ void step_finalize_kernel(StepDev* sd, double n_field, double lr0, do
 
 // Adam (bias-corrected), flat over every tensor; g is the raw dS/dtheta and is
 // scaled by 1/(N * n_total) here.  Writes the bf16 shadow of [sh_begin, sh_end).
+// Two float4 per array in flight per thread (memory-level parallelism).
+__device__ __forceinline__ void adam4(float4& pp, float4& mm, float4& vv, const float4& gg, float scale, float lr,
+                                      float c1, float c2, float b1, float b2, float eps) {
+  float* P = &pp.x; float* Mv = &mm.x; float* V = &vv.x; const float* G = &gg.x;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const float gr = G[c] * scale;
+    Mv[c] = b1 * Mv[c] + (1.f - b1) * gr;
+    V[c] = b2 * V[c] + (1.f - b2) * gr * gr;
+    P[c] = P[c] - lr * (Mv[c] / c1) / (sqrtf(V[c] / c2) + eps);
+  }
+}
+
+__device__ __forceinline__ void store_shadow(__nv_bfloat16* shadow, uint64_t e, uint64_t b0, uint64_t b1,
+                                             const float4& p) {
+  if (shadow && e >= b0 && e < b1) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(p.x, p.y);
+    __nv_bfloat162 hi = __floats2bfloat162_rn(p.z, p.w);
+    reinterpret_cast<uint2*>(shadow + (e - b0))[0] =
+        make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+  }
+}
+
 __global__ void __launch_bounds__(256)
 adam_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v, const float* __restrict__ g,
             uint64_t n4, const StepDev* __restrict__ sd, float b1, float b2, float eps,
             __nv_bfloat16* __restrict__ shadow, uint64_t sh_begin, uint64_t sh_end) {
   if (sd->skip) return;
   const float scale = sd->scale, lr = sd->lr, c1 = sd->c1, c2 = sd->c2;
-  const float ib1 = 1.f - b1, ib2 = 1.f - b2;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4; i += (uint64_t)gridDim.x * blockDim.x) {
-    float4 pp = reinterpret_cast<float4*>(p)[i];
-    float4 mm = reinterpret_cast<float4*>(m)[i];
-    float4 vv = reinterpret_cast<float4*>(v)[i];
-    const float4 gg = reinterpret_cast<const float4*>(g)[i];
-    float* P = &pp.x; float* Mv = &mm.x; float* V = &vv.x; const float* G = &gg.x;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const float gr = G[c] * scale;
-      Mv[c] = b1 * Mv[c] + ib1 * gr;
-      V[c] = b2 * V[c] + ib2 * gr * gr;
-      const float mh = Mv[c] / c1;
-      const float vh = V[c] / c2;
-      P[c] = P[c] - lr * mh / (sqrtf(vh) + eps);
-    }
-    reinterpret_cast<float4*>(p)[i] = pp;
-    reinterpret_cast<float4*>(m)[i] = mm;
-    reinterpret_cast<float4*>(v)[i] = vv;
-    const uint64_t e = 4 * i;
-    if (shadow && e >= sh_begin && e < sh_end) {
-      __nv_bfloat162 lo = __floats2bfloat162_rn(P[0], P[1]);
-      __nv_bfloat162 hi = __floats2bfloat162_rn(P[2], P[3]);
-      uint2 pk = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
-      reinterpret_cast<uint2*>(shadow + (e - sh_begin))[0] = pk;
-    }
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  float4* P4 = reinterpret_cast<float4*>(p);
+  float4* M4 = reinterpret_cast<float4*>(m);
+  float4* V4 = reinterpret_cast<float4*>(v);
+  const float4* G4 = reinterpret_cast<const float4*>(g);
+  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  for (; i + stride < n4; i += 2 * stride) {
+    const uint64_t j = i + stride;
+    float4 pa = P4[i], pb = P4[j], ma = M4[i], mb = M4[j], va = V4[i], vb = V4[j];
+    const float4 ga = __ldcs(G4 + i), gb = __ldcs(G4 + j);
+    adam4(pa, ma, va, ga, scale, lr, c1, c2, b1, b2, eps);
+    adam4(pb, mb, vb, gb, scale, lr, c1, c2, b1, b2, eps);
+    P4[i] = pa; P4[j] = pb; M4[i] = ma; M4[j] = mb; V4[i] = va; V4[j] = vb;
+    store_shadow(shadow, 4 * i, sh_begin, sh_end, pa);
+    store_shadow(shadow, 4 * j, sh_begin, sh_end, pb);
+  }
+  if (i < n4) {
+    float4 pa = P4[i], ma = M4[i], va = V4[i];
+    const float4 ga = G4[i];
+    adam4(pa, ma, va, ga, scale, lr, c1, c2, b1, b2, eps);
+    P4[i] = pa; M4[i] = ma; V4[i] = va;
+    store_shadow(shadow, 4 * i, sh_begin, sh_end, pa);
   }
 }
 
@@ -344,7 +363,7 @@ void step_finalize(StepDev* sd, double n_field, double lr0, double lr_min, uint6
 void adam_flat(float* p, float* m, float* v, const float* g, uint64_t n, const StepDev* sd, float b1, float b2,
                float eps, __nv_bfloat16* shadow, uint64_t sh_begin, uint64_t sh_end, cudaStream_t s) {
   const uint64_t n4 = n / 4;   // the flat buffer is padded to a multiple of 4
-  adam_kernel<<<grid_for(n4, 256, 148 * 8), 256, 0, s>>>(p, m, v, g, n4, sd, b1, b2, eps, shadow, sh_begin, sh_end);
+  adam_kernel<<<grid_for(n4, 256, 148 * 16), 256, 0, s>>>(p, m, v, g, n4, sd, b1, b2, eps, shadow, sh_begin, sh_end);
 }
 
 void init_tensor(float* dst, uint64_t count, uint32_t tid, uint32_t fan_in, uint64_t seed, cudaStream_t s) {
