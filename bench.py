@@ -36,7 +36,7 @@ CAP, THETA, BATCH = 6000, 1000, 1024
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--puts-per-step", type=int, default=4)
@@ -142,23 +142,27 @@ class Clocks:
         try:
             self.f = open(self.path, "w")
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + q, "--format=csv,noheader,nounits",
-                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
-            time.sleep(0.3)
+                                       "-lms", "20"], stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.5)
         except Exception:
             self.p = None
         return self
 
     def __exit__(self, *a):
         if self.p:
+            time.sleep(0.05)
             self.p.terminate()
             self.p.wait()
             self.f.close()
 
     def summary(self):
         try:
-            rows = [l.split(",") for l in open(self.path).read().strip().splitlines()]
-            sm = [float(r[1]) for r in rows if len(r) >= 9]
-            mx = max(float(r[2]) for r in rows if len(r) >= 9)
+            rows = [[x.strip() for x in l.split(",")] for l in open(self.path).read().strip().splitlines()]
+            rows = [r for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+            if not rows:
+                return {"error": "no nvidia-smi sample inside the timed region"}
+            sm = [float(r[1]) for r in rows]
+            mx = max(float(r[2]) for r in rows)
             reasons = set()
             for r in rows:
                 for name, v in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"], r[5:9]):
@@ -282,7 +286,13 @@ def main():
 
     if args.profile:
         if rank == 0:
-            print(json.dumps({"ms_per_step": ms_step, "value": value}), flush=True)
+            prof = ctx.debug_counters().reshape(160, 32)[:148].astype(np.float64)
+            names = {0: "mma_total", 1: "mma_w_full", 2: "mma_h_full", 3: "mma_y_empty", 4: "mma_dy_full",
+                     5: "mma_dw_empty", 8: "epi_total", 9: "epi_t_full", 10: "epi_y_full", 11: "epi_dy_empty",
+                     12: "epi_store_bar", 13: "epi_dw_readout", 14: "epi_db_bar", 16: "tma_total", 17: "tma_w_empty",
+                     18: "tma_h_empty", 24: "ld_total", 25: "ld_t_empty"}
+            k1 = {v: float(prof[:, k].mean()) for k, v in names.items()}
+            print(json.dumps({"ms_per_step": ms_step, "value": value, "k1_wait_cycles_mean_per_cta": k1}), flush=True)
         return 0
     # ---- per-kernel timing pass (CUDA events around each kernel class) ----
     ctx.set_flags(mel.FLAG_TIMING)

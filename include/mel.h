@@ -222,6 +222,9 @@ int mel_kernel_time(mel_ctx* ctx, int k, double* ms_host, uint64_t* launches_hos
 int mel_kernel_time_reset(mel_ctx* ctx);
 /* Replaces cfg.flags (MEL_FLAG_*) from the next call on.  Always MEL_OK. */
 int mel_set_flags(mel_ctx* ctx, uint32_t flags);
+/* Diagnostic: per-CTA wait-cycle counters of the output-layer kernel's warp roles
+ * (layout documented in csrc/tc_out.cu).  Copies up to n uint64 values. */
+int mel_debug_counters(mel_ctx* ctx, uint64_t* out_host, int n);
 /* Number of library kernel launches since creation (bench "gpu_launches"). */
 int mel_launch_count(const mel_ctx* ctx, uint64_t* n_host);
 

@@ -513,7 +513,8 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
     c->max_parts = tc::max_sse_parts(c->Npad);
     DALLOC(c->d_sse_part, c->max_parts);
     to_bf16(c->d_p + c->off[2 * (c->L - 1)], c->d_shadow[0], c->Npad * c->Klast, c->stream);
-    r = tc::prepare(c->tcb, c->Npad, c->B, c->Klast, c->d_shadow[0]);
+    r = tc::prepare(c->tcb, c->Npad, c->B, c->Klast, c->d_shadow[0],
+                    static_cast<const __nv_bfloat16*>(c->ra.payload), c->C, c->d_g + c->off[2 * (c->L - 1)]);
     if (r) return fail(c, MEL_ECUDA, "tensor-core kernel setup failed: %s", tc::last_error());
   }
   r = check_launch(c, "create");
@@ -911,6 +912,15 @@ int mel_kernel_time_reset(mel_ctx* c) {
   if (r) return r;
   drain_timers(c);
   for (int k = 0; k < MEL_K_COUNT; ++k) { c->kms[k] = 0; c->klaunch[k] = 0; }
+  return MEL_OK;
+}
+
+int mel_debug_counters(mel_ctx* c, uint64_t* out, int n) {
+  GUARD(c);
+  if (!out || n <= 0) return fail(c, MEL_EINVAL, "bad counter buffer");
+  int r = sync_stream(c);
+  if (r) return r;
+  if (tc::read_k1_profile(reinterpret_cast<unsigned long long*>(out), n)) return fail(c, MEL_ECUDA, "counter read failed");
   return MEL_OK;
 }
 

@@ -210,15 +210,17 @@ __global__ void step_finalize_kernel(StepDev* sd, double n_field, double lr0, do
 // Adam (bias-corrected), flat over every tensor; g is the raw dS/dtheta and is
 // scaled by 1/(N * n_total) here.  Writes the bf16 shadow of [sh_begin, sh_end).
 // Two float4 per array in flight per thread (memory-level parallelism).
-__device__ __forceinline__ void adam4(float4& pp, float4& mm, float4& vv, const float4& gg, float scale, float lr,
-                                      float c1, float c2, float b1, float b2, float eps) {
+__device__ __forceinline__ void adam4(float4& pp, float4& mm, float4& vv, const float4& gg, float scale, float step,
+                                      float inv_sqrt_c2, float b1, float b2, float eps) {
+  // PyTorch form: denom = sqrt(v) / sqrt(1 - b2^k) + eps;  p -= (lr / (1 - b1^k)) * m / denom
   float* P = &pp.x; float* Mv = &mm.x; float* V = &vv.x; const float* G = &gg.x;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const float gr = G[c] * scale;
-    Mv[c] = b1 * Mv[c] + (1.f - b1) * gr;
-    V[c] = b2 * V[c] + (1.f - b2) * gr * gr;
-    P[c] = P[c] - lr * (Mv[c] / c1) / (sqrtf(V[c] / c2) + eps);
+    Mv[c] = fmaf(b1, Mv[c], (1.f - b1) * gr);
+    V[c] = fmaf(b2, V[c], (1.f - b2) * gr * gr);
+    const float denom = fmaf(__fsqrt_rn(V[c]), inv_sqrt_c2, eps);
+    P[c] = fmaf(-step, __fdiv_rn(Mv[c], denom), P[c]);
   }
 }
 
@@ -237,7 +239,7 @@ adam_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
             uint64_t n4, const StepDev* __restrict__ sd, float b1, float b2, float eps,
             __nv_bfloat16* __restrict__ shadow, uint64_t sh_begin, uint64_t sh_end) {
   if (sd->skip) return;
-  const float scale = sd->scale, lr = sd->lr, c1 = sd->c1, c2 = sd->c2;
+  const float scale = sd->scale, step = sd->lr / sd->c1, isc2 = rsqrtf(sd->c2);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   float4* P4 = reinterpret_cast<float4*>(p);
   float4* M4 = reinterpret_cast<float4*>(m);
@@ -248,8 +250,8 @@ adam_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
     const uint64_t j = i + stride;
     float4 pa = P4[i], pb = P4[j], ma = M4[i], mb = M4[j], va = V4[i], vb = V4[j];
     const float4 ga = __ldcs(G4 + i), gb = __ldcs(G4 + j);
-    adam4(pa, ma, va, ga, scale, lr, c1, c2, b1, b2, eps);
-    adam4(pb, mb, vb, gb, scale, lr, c1, c2, b1, b2, eps);
+    adam4(pa, ma, va, ga, scale, step, isc2, b1, b2, eps);
+    adam4(pb, mb, vb, gb, scale, step, isc2, b1, b2, eps);
     P4[i] = pa; P4[j] = pb; M4[i] = ma; M4[j] = mb; V4[i] = va; V4[j] = vb;
     store_shadow(shadow, 4 * i, sh_begin, sh_end, pa);
     store_shadow(shadow, 4 * j, sh_begin, sh_end, pb);
@@ -257,7 +259,7 @@ adam_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
   if (i < n4) {
     float4 pa = P4[i], ma = M4[i], va = V4[i];
     const float4 ga = G4[i];
-    adam4(pa, ma, va, ga, scale, lr, c1, c2, b1, b2, eps);
+    adam4(pa, ma, va, ga, scale, step, isc2, b1, b2, eps);
     P4[i] = pa; M4[i] = ma; V4[i] = va;
     store_shadow(shadow, 4 * i, sh_begin, sh_end, pa);
   }

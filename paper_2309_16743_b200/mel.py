@@ -27,7 +27,7 @@ EXPORTS = ["mel_config_default", "mel_nccl_unique_id", "mel_create", "mel_destro
            "mel_param_layout", "mel_set_params", "mel_get_params", "mel_get_state", "mel_set_state",
            "reservoir_put", "reservoir_close", "reservoir_sample_batch", "surrogate_step", "surrogate_eval",
            "reservoir_stats", "reservoir_dump", "mel_sync", "mel_kernel_time", "mel_kernel_time_reset",
-           "mel_launch_count", "mel_set_flags"]
+           "mel_launch_count", "mel_set_flags", "mel_debug_counters"]
 
 
 class MelError(RuntimeError):
@@ -93,6 +93,7 @@ def load_library(path: str = LIB_PATH):
         "mel_kernel_time_reset": (C.c_int, [vp]),
         "mel_launch_count": (C.c_int, [vp, C.POINTER(u64)]),
         "mel_set_flags": (C.c_int, [vp, u32]),
+        "mel_debug_counters": (C.c_int, [vp, C.POINTER(u64), C.c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -297,6 +298,11 @@ class Context:
 
     def kernel_time_reset(self):
         self._check(self.lib.mel_kernel_time_reset(self.h))
+
+    def debug_counters(self, n: int = 160 * 32):
+        out = np.zeros(n, dtype=np.uint64)
+        self._check(self.lib.mel_debug_counters(self.h, out.ctypes.data_as(C.POINTER(C.c_uint64)), n))
+        return out
 
     def set_flags(self, flags: int):
         self._check(self.lib.mel_set_flags(self.h, flags))
