@@ -211,7 +211,7 @@ def main():
     # synthetic ensemble: exact heat solutions by linearity from a GPU-generated basis
     phi = heat_torch.basis(args.grid, TAU, device=dev)                       # (5, tau, N) fp32
     Xd = torch.from_numpy(design.draw_design(SIMS, seed=1)).to(dev)
-    order = [(s, t) for s in range(SIMS) for t in range(TAU) if (s + t) % world == rank]
+    order = design.routed_stream(SIMS, TAU, rank, world)
     cursor = [0]
 
     def next_batch(n):

@@ -95,3 +95,9 @@ def build_oplog(wl: Workload, n_steps_after_close: int | None = None,
             ops.append(("SAMPLE", r))
         ops.append(("STEP",))
     return ops
+
+
+def routed_stream(n_sims: int, tau: int, rank: int, world: int) -> list[tuple[int, int]]:
+    """The (sim, t) time steps one server rank receives, in arrival order: the
+    global stream (sims in order, t ascending) filtered by the round-robin route."""
+    return [(s, t) for s in range(n_sims) for t in range(tau) if route(s, t, world) == rank]
