@@ -85,6 +85,8 @@ void launch_init_res(const ResArgs& a, cudaStream_t s);
 enum Epi { EPI_STORE = 0, EPI_BIAS_RELU = 1, EPI_BIAS = 2 };
 void sgemm(bool ta, bool tb, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
            float* C, int ldc, int epi, const float* bias, float* H, int ldh, int splits, cudaStream_t s);
+int sgemm_auto(bool ta, bool tb, int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
+               int epi, const float* bias, float* H, int ldh, float* scratch, size_t scratch_elems, cudaStream_t s);
 void splitk_reduce(int M, int N, int splits, const float* part, float* C, int ldc, const float* relu_mask,
                    int ldm, cudaStream_t s);
 struct OutArgs {

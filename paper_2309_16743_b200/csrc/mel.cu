@@ -248,14 +248,8 @@ int world_allreduce(mel_ctx* c) {
   return MEL_OK;
 }
 
-int head_splits(uint32_t B, uint64_t out_elems, size_t part_elems) {
-  int sk = (int)(B / 128);
-  if (sk > 16) sk = 16;
-  while (sk > 1 && (size_t)sk * out_elems > part_elems) --sk;
-  return sk < 1 ? 1 : sk;
-}
-
-// backward of the head layers given dZ of the last hidden layer (d_dz[L-2])
+// backward of the head layers given dZ of the last hidden layer (d_dz[L-2]); every
+// GEMM is split-K through the partial buffer when its grid is below one wave
 int head_backward(mel_ctx* c) {
   const int L = c->L;
   Timer t(c, MEL_K_HEAD_BWD, 0);
@@ -267,25 +261,16 @@ int head_backward(mel_ctx* c) {
     const int ldin = (l == 1) ? 8 : din;
     float* gW = c->d_g + c->off[2 * (l - 1)];
     float* gb = c->d_g + c->off[2 * (l - 1) + 1];
-    // dW = dZ^T H_in reduces over the batch: split-K so the tiny output grid fills the SMs
-    const int sk = head_splits(c->B, (uint64_t)dout * din, c->part_elems);
-    if (sk > 1) {
-      sgemm(true, false, dout, din, (int)c->B, dZ, dout, Hin, ldin, c->d_part, din, EPI_STORE, nullptr, nullptr, 0,
-            sk, c->stream);
-      splitk_reduce(dout, din, sk, c->d_part, gW, din, nullptr, 0, c->stream);
-      ++nl;
-    } else {
-      sgemm(true, false, dout, din, (int)c->B, dZ, dout, Hin, ldin, gW, din, EPI_STORE, nullptr, nullptr, 0, 1,
-            c->stream);
-    }
+    nl += sgemm_auto(true, false, dout, din, (int)c->B, dZ, dout, Hin, ldin, gW, din, EPI_STORE, nullptr, nullptr, 0,
+                     c->d_part, c->part_elems, c->stream);
     col_sum(dZ, (int)c->B, dout, dout, gb, c->stream);
-    nl += 2;
+    nl += 1;
     if (l > 1) {
-      nl += 2;
       const float* W = c->d_p + c->off[2 * (l - 1)];
-      sgemm(false, false, (int)c->B, din, dout, dZ, dout, W, din, c->d_dz[l - 2], din, EPI_STORE, nullptr, nullptr, 0, 1,
-            c->stream);
+      nl += sgemm_auto(false, false, (int)c->B, din, dout, dZ, dout, W, din, c->d_dz[l - 2], din, EPI_STORE, nullptr,
+                       nullptr, 0, c->d_part, c->part_elems, c->stream);
       relu_mask_mul(c->d_dz[l - 2], c->d_z[l - 2], (uint64_t)c->B * din, c->stream);
+      nl += 1;
     }
   }
   c->launches += nl;
@@ -294,14 +279,16 @@ int head_backward(mel_ctx* c) {
 }
 
 int head_forward(mel_ctx* c, const float* xn, float** Z, float** H, int rows) {
+  int nl = 0;
   for (int l = 1; l < c->L; ++l) {
     const int din = c->dims[l - 1], dout = c->dims[l];
     const float* Hin = (l == 1) ? xn : H[l - 2];
     const int ldin = (l == 1) ? 8 : din;
-    sgemm(false, true, rows, dout, din, Hin, ldin, c->d_p + c->off[2 * (l - 1)], din, Z[l - 1], dout, EPI_BIAS_RELU,
-          c->d_p + c->off[2 * (l - 1) + 1], H[l - 1], dout, 1, c->stream);
+    nl += sgemm_auto(false, true, rows, dout, din, Hin, ldin, c->d_p + c->off[2 * (l - 1)], din, Z[l - 1], dout,
+                     EPI_BIAS_RELU, c->d_p + c->off[2 * (l - 1) + 1], H[l - 1], dout, c->d_part, c->part_elems,
+                     c->stream);
   }
-  return MEL_OK;
+  return nl;
 }
 
 int splits_for(uint64_t K) {
@@ -739,8 +726,10 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
     launch_gather(c->ra, c->d_slots, c->B, c->cfg.steps_per_sim, c->d_xn, c->stream);
   }
   {
-    Timer t(c, MEL_K_HEAD_FWD, c->L - 1);
-    head_forward(c, c->d_xn, c->d_z, c->d_h, (int)c->B);
+    Timer t(c, MEL_K_HEAD_FWD, 0);
+    const int nl = head_forward(c, c->d_xn, c->d_z, c->d_h, (int)c->B);
+    c->launches += nl;
+    c->klaunch[MEL_K_HEAD_FWD] += nl;
   }
   if ((r = check_launch(c, "head forward"))) return r;
   r = c->cfg.precision == MEL_FP32 ? train_step_fp32(c) : train_step_bf16(c);

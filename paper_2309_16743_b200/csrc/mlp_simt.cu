@@ -158,12 +158,40 @@ out_fwd_f32_kernel(OutArgs a) {
   if (threadIdx.x == 0) a.sse_part[blockIdx.y * gridDim.x + blockIdx.x] = s_red[0];
 }
 
-__global__ void col_sum_kernel(const float* __restrict__ X, int rows, int cols, int ld, float* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= cols) return;
+// column sums over the batch: 32 columns x 8 row-groups per block, each thread a
+// fixed strided order, then the 8 partials in fixed order (deterministic)
+__global__ void __launch_bounds__(256)
+col_sum_kernel(const float* __restrict__ X, int rows, int cols, int ld, float* __restrict__ out) {
+  __shared__ float part[8][33];
+  const int cl = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cl;
   float s = 0.f;
-  for (int r = 0; r < rows; ++r) s += X[(size_t)r * ld + c];   // fixed order over the batch
-  out[c] = s;
+  if (c < cols)
+    for (int r = grp; r < rows; r += 8) s += X[(size_t)r * ld + c];
+  part[grp][cl] = s;
+  __syncthreads();
+  if (grp == 0 && c < cols) {
+    float t = 0.f;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) t += part[g][cl];
+    out[c] = t;
+  }
+}
+
+// split-K reduction with the GEMM epilogues: out = sum_z part[z] (+ bias, then Z/H
+// with ReLU for EPI_BIAS_RELU), fixed order over z
+__global__ void splitk_reduce_epi_kernel(int M, int N, int splits, const float* __restrict__ part, float* __restrict__ C,
+                                         int ldc, int epi, const float* __restrict__ bias, float* __restrict__ H,
+                                         int ldh) {
+  const size_t total = (size_t)M * N;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i / N), n = (int)(i % N);
+    float v = 0.f;
+    for (int z = 0; z < splits; ++z) v += part[(size_t)z * M * N + i];
+    if (epi != EPI_STORE) v += bias[n];
+    C[(size_t)m * ldc + n] = v;
+    if (epi == EPI_BIAS_RELU) H[(size_t)m * ldh + n] = fmaxf(v, 0.f);
+  }
 }
 
 __global__ void reduce_local_kernel(StepDev* sd, const double* parts, int n_parts, const ResDev* st) {
@@ -350,7 +378,23 @@ int out_fwd_f32(const OutArgs& a, cudaStream_t s) {
 }
 
 void col_sum(const float* X, int rows, int cols, int ld, float* out, cudaStream_t s) {
-  col_sum_kernel<<<(cols + 255) / 256, 256, 0, s>>>(X, rows, cols, ld, out);
+  col_sum_kernel<<<(cols + 31) / 32, 256, 0, s>>>(X, rows, cols, ld, out);
+}
+
+// SIMT GEMM that fills the GPU: split-K through `scratch` (>= splits*M*N floats) when
+// the output grid is smaller than one wave; returns the number of launches
+int sgemm_auto(bool ta, bool tb, int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
+               int epi, const float* bias, float* H, int ldh, float* scratch, size_t scratch_elems, cudaStream_t s) {
+  const int tiles = ((M + TM - 1) / TM) * ((N + TN - 1) / TN);
+  int sk = 1;
+  while (tiles * sk < 148 && K / (sk * 2) >= 64 && (size_t)(sk * 2) * M * N <= scratch_elems) sk *= 2;
+  if (sk == 1) {
+    sgemm(ta, tb, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, 1, s);
+    return 1;
+  }
+  sgemm(ta, tb, M, N, K, A, lda, B, ldb, scratch, N, EPI_STORE, nullptr, nullptr, 0, sk, s);
+  splitk_reduce_epi_kernel<<<grid_for((uint64_t)M * N), 256, 0, s>>>(M, N, sk, scratch, C, ldc, epi, bias, H, ldh);
+  return 2;
 }
 
 void reduce_local(StepDev* sd, const double* parts, int n_parts, const ResDev* st, cudaStream_t s) {
