@@ -95,6 +95,8 @@ typedef struct {
 } mel_config;
 
 #define MEL_FLAG_TIMING 1u     /* record CUDA events around every kernel (bench roofline) */
+#define MEL_FLAG_NO_ZERO 2u    /* world > 1, bf16: plain all-reduce + replicated Adam instead of
+                                  reduce-scatter / sharded Adam / shadow all-gather            */
 
 typedef struct {
   uint64_t population, unseen, seen;     /* p, u, s = p - u                            */
@@ -138,13 +140,14 @@ int mel_param_layout(const mel_ctx* ctx, uint32_t* n_tensors, uint32_t* shapes /
                      uint64_t* total);
 
 /* Host fp32 parameters in / out (tensor order above).  set: all ranks must set
- * identical values; resets nothing else.  get synchronises the stream. */
+ * identical values; resets nothing else.  get synchronises the stream; with world > 1
+ * in bf16 mode (row-sharded W_L optimiser state) get is COLLECTIVE (all-gather). */
 int mel_set_params(mel_ctx* ctx, const float* const* tensors_host);
 int mel_get_params(mel_ctx* ctx, float* const* tensors_host);
 
 /* Full optimiser state (params, Adam first/second moments, step count k and
  * global samples S), host fp32.  Used by checkpointing and by the re-anchored
- * parity harness.  Synchronises. */
+ * parity harness.  Synchronises; COLLECTIVE with world > 1 in bf16 mode. */
 typedef struct {
   float* const* p;
   float* const* m;
@@ -195,7 +198,7 @@ int surrogate_step(mel_ctx* ctx, double* loss_host);
  * kelvin, t_host n, fields_host n x N fp32 kelvin (nullable: then no MSE).
  * mse_host (nullable) receives the MSE in normalised units (reading Q13);
  * pred_host (nullable, n x N) the predictions de-normalised to kelvin.
- * Synchronises. */
+ * Synchronises; COLLECTIVE with world > 1 in bf16 mode (gathers the W_L master). */
 int surrogate_eval(mel_ctx* ctx, const float* X_host, const uint32_t* t_host,
                    const float* fields_host, uint32_t n, double* mse_host, float* pred_host);
 

@@ -81,6 +81,14 @@ struct mel_ctx {
   float *d_eval_z[2] = {nullptr, nullptr}, *d_eval_h[2] = {nullptr, nullptr}; float* d_eval_xn = nullptr;
 
   ncclComm_t comm = nullptr;
+  // ZeRO-1 style exchange (world > 1, bf16 mode): reduce-scatter of dW_L on a comm
+  // stream overlapped with the rest of the backward, Adam on this rank's W_L row
+  // shard, all-gather of the bf16 shadow
+  bool zero = false;
+  uint64_t shard_elems = 0, shard_off = 0;   // W_L elements per rank, this rank's offset in W_L
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_gw = nullptr, ev_head = nullptr, ev_ar = nullptr, ev_adam = nullptr, ev_ag = nullptr;
+  bool ag_pending = false;
 
   // timing
   std::vector<TimedPair> pending;
@@ -156,16 +164,16 @@ cudaEvent_t take_event(mel_ctx* c) {
 
 // RAII-free timing brackets around one launch group of kernel class k
 struct Timer {
-  mel_ctx* c; int k; cudaEvent_t a = nullptr;
-  Timer(mel_ctx* c_, int k_, int nlaunch) : c(c_), k(k_) {
+  mel_ctx* c; int k; cudaEvent_t a = nullptr; cudaStream_t st;
+  Timer(mel_ctx* c_, int k_, int nlaunch, cudaStream_t s_ = nullptr) : c(c_), k(k_), st(s_ ? s_ : c_->stream) {
     c->launches += nlaunch;
     c->klaunch[k] += nlaunch;
-    if (c->cfg.flags & MEL_FLAG_TIMING) { a = take_event(c); cudaEventRecord(a, c->stream); }
+    if (c->cfg.flags & MEL_FLAG_TIMING) { a = take_event(c); cudaEventRecord(a, st); }
   }
   ~Timer() {
     if (a) {
       cudaEvent_t b = take_event(c);
-      cudaEventRecord(b, c->stream);
+      cudaEventRecord(b, st);
       c->pending.push_back({k, a, b});
     }
   }
@@ -238,13 +246,70 @@ int commit(mel_ctx* c) {
   return check_launch(c, "commit");
 }
 
-int world_allreduce(mel_ctx* c) {
+// Gradient exchange (the locally computed gradients are all-reduced so that
+// every replica applies the same mean update).  Plain mode: one grouped all-reduce of
+// the flat fp32 gradients + [SSE, n].  ZeRO mode: the W_L gradient is reduce-scattered
+// on the comm stream as soon as K1 has written it (overlapping K2 and the head
+// backward); the small region (head weights, every bias) and [SSE, n] are
+// all-reduced after the head backward.  Same sums, same mean update.
+int world_exchange(mel_ctx* c) {
   if (c->world == 1) return MEL_OK;
-  Timer t(c, MEL_K_ALLREDUCE, 0);
+  if (!c->zero) {
+    Timer t(c, MEL_K_ALLREDUCE, 0);
+    NK(ncclGroupStart());
+    NK(ncclAllReduce(c->d_g, c->d_g, c->n_flat, ncclFloat32, ncclSum, c->comm, c->stream));
+    NK(ncclAllReduce(c->d_sd->red, c->d_sd->red, 2, ncclFloat64, ncclSum, c->comm, c->stream));
+    NK(ncclGroupEnd());
+    return MEL_OK;
+  }
+  const uint64_t offW = c->off[2 * (c->L - 1)];
+  CK(cudaEventRecord(c->ev_head, c->stream));
+  {
+    Timer t(c, MEL_K_ALLREDUCE, 0, c->comm_stream);
+    CK(cudaStreamWaitEvent(c->comm_stream, c->ev_gw, 0));
+    float* gW = c->d_g + offW;
+    NK(ncclReduceScatter(gW, gW + c->shard_off, c->shard_elems, ncclFloat32, ncclSum, c->comm, c->comm_stream));
+    CK(cudaStreamWaitEvent(c->comm_stream, c->ev_head, 0));
+    NK(ncclGroupStart());
+    NK(ncclAllReduce(c->d_g, c->d_g, offW, ncclFloat32, ncclSum, c->comm, c->comm_stream));
+    NK(ncclAllReduce(c->d_sd->red, c->d_sd->red, 2, ncclFloat64, ncclSum, c->comm, c->comm_stream));
+    NK(ncclGroupEnd());
+    CK(cudaEventRecord(c->ev_ar, c->comm_stream));
+  }
+  CK(cudaStreamWaitEvent(c->stream, c->ev_ar, 0));
+  return MEL_OK;
+}
+
+// all-gather of a W_L-shaped buffer from the row shards (collective, comm stream)
+int gather_shards(mel_ctx* c, void* base, size_t esz, ncclDataType_t ty) {
+  char* b = static_cast<char*>(base);
+  NK(ncclAllGather(b + c->shard_off * esz, b, c->shard_elems, ty, c->comm, c->comm_stream));
+  return MEL_OK;
+}
+
+// wait (device-side) for the pending shadow all-gather before anything reads W_L
+int wait_shadow(mel_ctx* c) {
+  if (c->ag_pending) {
+    CK(cudaStreamWaitEvent(c->stream, c->ev_ag, 0));
+    c->ag_pending = false;
+  }
+  return MEL_OK;
+}
+
+// full fp32 W_L master (and moments) on every rank, for host reads (collective)
+int gather_master(mel_ctx* c, bool moments) {
+  if (!c->zero) return MEL_OK;
+  const uint64_t offW = c->off[2 * (c->L - 1)];
+  CK(cudaEventRecord(c->ev_head, c->stream));
+  CK(cudaStreamWaitEvent(c->comm_stream, c->ev_head, 0));
   NK(ncclGroupStart());
-  NK(ncclAllReduce(c->d_g, c->d_g, c->n_flat, ncclFloat32, ncclSum, c->comm, c->stream));
-  NK(ncclAllReduce(c->d_sd->red, c->d_sd->red, 2, ncclFloat64, ncclSum, c->comm, c->stream));
+  int r = gather_shards(c, c->d_p + offW, 4, ncclFloat32);
+  if (!r && moments) r = gather_shards(c, c->d_m + offW, 4, ncclFloat32);
+  if (!r && moments) r = gather_shards(c, c->d_v + offW, 4, ncclFloat32);
   NK(ncclGroupEnd());
+  if (r) return r;
+  CK(cudaEventRecord(c->ev_ar, c->comm_stream));
+  CK(cudaStreamWaitEvent(c->stream, c->ev_ar, 0));
   return MEL_OK;
 }
 
@@ -315,6 +380,7 @@ int train_step_fp32(mel_ctx* c) {
           (int)K, EPI_STORE, nullptr, nullptr, 0, 1, c->stream);
     col_sum(c->d_dy, (int)B, (int)c->Npad, (int)c->Npad, c->d_g + c->off[2 * (L - 1) + 1], c->stream);
   }
+  if (c->zero) CK(cudaEventRecord(c->ev_gw, c->stream));
   {
     Timer t(c, MEL_K_OUT_DH, 2);
     // dH = dY W  (M = B, N = K, K = Npad), split-K, then ReLU' mask -> dZ_{L-1}
@@ -351,10 +417,13 @@ int train_step_bf16(mel_ctx* c) {
   a.dz = c->d_dz[L - 2];
   a.z = c->d_z[L - 2];
   int nparts = 0;
+  int r0 = wait_shadow(c);
+  if (r0) return r0;
   {
     Timer t(c, MEL_K_OUT_FWD_DW, 1);
     nparts = tc::launch_out_fwd_dw(a, c->tcb, c->stream);
   }
+  if (c->zero) CK(cudaEventRecord(c->ev_gw, c->stream));
   {
     Timer t(c, MEL_K_OUT_DH, 2);
     tc::launch_out_dh(a, c->tcb, c->stream);
@@ -416,16 +485,25 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
   c->dims[nd++] = g->n_field;
   c->L = nd - 1;
   c->N = g->n_field; c->B = g->batch; c->C = g->capacity;
-  c->Npad = ((uint64_t)c->N + 127) / 128 * 128;
+  // rows of W_L padded to 128 (UMMA M) x world (equal row shards under ZeRO)
+  const uint64_t row_quant = 128ull * (uint64_t)c->world;
+  c->Npad = ((uint64_t)c->N + row_quant - 1) / row_quant * row_quant;
   c->Klast = c->dims[c->L - 1];
   c->hmax = g->hidden[0] > g->hidden[1] ? g->hidden[0] : g->hidden[1];
+  // flat layout: W_1 b_1 ... W_{L-1} b_{L-1} b_L W_L, i.e. everything but W_L forms one
+  // small contiguous region [0, off(W_L)) (replicated under ZeRO), tensors 64-B aligned
   uint64_t o = 0;
   for (int l = 0; l < c->L; ++l) {
     const uint64_t rows = (l == c->L - 1) ? c->Npad : c->dims[l + 1];
-    c->off[2 * l] = o; c->cnt[2 * l] = rows * c->dims[l];
-    o += (c->cnt[2 * l] + 15) / 16 * 16;
-    c->off[2 * l + 1] = o; c->cnt[2 * l + 1] = rows;
-    o += (rows + 15) / 16 * 16;
+    c->cnt[2 * l] = rows * c->dims[l];
+    c->cnt[2 * l + 1] = rows;
+    if (l < c->L - 1) {
+      c->off[2 * l] = o; o += (c->cnt[2 * l] + 15) / 16 * 16;
+      c->off[2 * l + 1] = o; o += (rows + 15) / 16 * 16;
+    } else {
+      c->off[2 * l + 1] = o; o += (rows + 15) / 16 * 16;
+      c->off[2 * l] = o; o += (c->cnt[2 * l] + 15) / 16 * 16;
+    }
   }
   c->n_flat = o;
 
@@ -512,6 +590,12 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
     ncclUniqueId id;
     memcpy(&id, nccl_id, sizeof id);
     NK(ncclCommInitRank(&c->comm, c->world, id, c->rank));
+    c->zero = (g->precision == MEL_BF16) && !(g->flags & MEL_FLAG_NO_ZERO);
+    c->shard_elems = c->Npad / c->world * c->Klast;
+    c->shard_off = (uint64_t)c->rank * c->shard_elems;
+    CK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    cudaEvent_t* evs[] = {&c->ev_gw, &c->ev_head, &c->ev_ar, &c->ev_adam, &c->ev_ag};
+    for (cudaEvent_t* e : evs) CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   }
   return MEL_OK;
 }
@@ -538,7 +622,12 @@ void mel_destroy(mel_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->dev);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
   if (c->comm) ncclCommDestroy(c->comm);
+  cudaEvent_t evs[] = {c->ev_gw, c->ev_head, c->ev_ar, c->ev_adam, c->ev_ag};
+  for (cudaEvent_t e : evs)
+    if (e) cudaEventDestroy(e);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   drain_timers(c);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   void* ptrs[] = {c->d_st, (void*)c->ra.st_meta, (void*)c->ra.st_field, c->ra.meta, c->ra.seen, c->ra.put_seq,
@@ -586,6 +675,8 @@ static int copy_tensors(mel_ctx* c, float* base, float* const* host, bool to_hos
 }
 
 static int refresh_shadow(mel_ctx* c) {
+  int r0 = wait_shadow(c);
+  if (r0) return r0;
   if (c->cfg.precision == MEL_BF16)
     to_bf16(c->d_p + c->off[2 * (c->L - 1)], c->d_shadow[c->shadow_cur], c->Npad * c->Klast, c->stream);
   return check_launch(c, "shadow");
@@ -605,7 +696,9 @@ int mel_set_params(mel_ctx* c, const float* const* t) {
 int mel_get_params(mel_ctx* c, float* const* t) {
   GUARD(c);
   if (!t) return fail(c, MEL_EINVAL, "null tensors");
-  int r = copy_tensors(c, c->d_p, t, true);
+  int r = gather_master(c, false);
+  if (r) return r;
+  r = copy_tensors(c, c->d_p, t, true);
   if (r) return r;
   CK(cudaStreamSynchronize(c->stream));
   return MEL_OK;
@@ -614,7 +707,8 @@ int mel_get_params(mel_ctx* c, float* const* t) {
 int mel_get_state(mel_ctx* c, mel_state_view* s) {
   GUARD(c);
   if (!s) return fail(c, MEL_EINVAL, "null state");
-  int r;
+  int r = gather_master(c, true);
+  if (r) return r;
   if (s->p && (r = copy_tensors(c, c->d_p, s->p, true))) return r;
   if (s->m && (r = copy_tensors(c, c->d_m, s->m, true))) return r;
   if (s->v && (r = copy_tensors(c, c->d_v, s->v, true))) return r;
@@ -735,13 +829,22 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
   r = c->cfg.precision == MEL_FP32 ? train_step_fp32(c) : train_step_bf16(c);
   if (r) return r;
   if ((r = head_backward(c))) return r;
-  if ((r = world_allreduce(c))) return r;
+  if ((r = world_exchange(c))) return r;
   {
     Timer t(c, MEL_K_LOSS, 1);
     step_finalize(c->d_sd, (double)c->N, c->cfg.lr0, c->cfg.lr_min, c->cfg.lr_halving_samples, c->cfg.beta1,
                   c->cfg.beta2, c->d_mirror, c->d_st, c->stream);
   }
-  {
+  if (c->zero) {
+    // small region (head weights, every bias) replicated; W_L on this rank's row shard,
+    // refreshing the shard of the bf16 shadow, then all-gather of the shadow
+    Timer t(c, MEL_K_ADAM, 2);
+    const uint64_t offW = c->off[2 * (c->L - 1)], so = offW + c->shard_off;
+    const float b1 = (float)c->cfg.beta1, b2 = (float)c->cfg.beta2, eps = (float)c->cfg.eps;
+    adam_flat(c->d_p, c->d_m, c->d_v, c->d_g, offW, c->d_sd, b1, b2, eps, nullptr, 0, 0, c->stream);
+    adam_flat(c->d_p + so, c->d_m + so, c->d_v + so, c->d_g + so, c->shard_elems, c->d_sd, b1, b2, eps,
+              c->d_shadow[0] + c->shard_off, 0, c->shard_elems, c->stream);
+  } else {
     Timer t(c, MEL_K_ADAM, 1);
     __nv_bfloat16* sh = nullptr;
     uint64_t b0 = 0, b1 = 0;
@@ -754,6 +857,14 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
     }
     adam_flat(c->d_p, c->d_m, c->d_v, c->d_g, c->n_flat, c->d_sd, (float)c->cfg.beta1, (float)c->cfg.beta2,
               (float)c->cfg.eps, sh, b0, b1, c->stream);
+  }
+  if (c->zero) {
+    Timer t(c, MEL_K_ALLREDUCE, 0, c->comm_stream);
+    CK(cudaEventRecord(c->ev_adam, c->stream));
+    CK(cudaStreamWaitEvent(c->comm_stream, c->ev_adam, 0));
+    if ((r = gather_shards(c, c->d_shadow[0], 2, ncclBfloat16))) return r;
+    CK(cudaEventRecord(c->ev_ag, c->comm_stream));
+    c->ag_pending = true;
   }
   if ((r = check_launch(c, "adam"))) return r;
   c->batch_known = false;
@@ -787,6 +898,8 @@ int surrogate_eval(mel_ctx* c, const float* X, const uint32_t* t, const float* f
                    float* pred) {
   GUARD(c);
   if (!X || !t || n == 0) return fail(c, MEL_EINVAL, "bad eval arguments");
+  int rg = gather_master(c, false);   // full fp32 W_L (collective under ZeRO)
+  if (rg) return rg;
   const uint32_t chunk = c->B;
   if (!c->d_eval_x) {
     DALLOC(c->d_eval_x, (size_t)chunk * 5); DALLOC(c->d_eval_t, chunk); DALLOC(c->d_eval_xn, (size_t)chunk * 8);
@@ -881,6 +994,7 @@ int reservoir_dump(mel_ctx* c, uint32_t* sim, uint32_t* t, float* X, uint32_t* s
 
 int mel_sync(mel_ctx* c) {
   GUARD(c);
+  if (c->comm_stream) CK(cudaStreamSynchronize(c->comm_stream));
   return sync_stream(c);
 }
 
