@@ -104,6 +104,8 @@ void col_sum(const float* X, int rows, int cols, int ld, float* out, cudaStream_
 void reduce_local(StepDev* sd, const double* parts, int n_parts, const ResDev* st, cudaStream_t s);
 void step_finalize(StepDev* sd, double n_field, double lr0, double lr_min, uint64_t halving, double b1, double b2,
                    Mirror* mirror, ResDev* st, cudaStream_t s);
+void step_prepare(StepDev* sd, const ResDev* st, double n_field, double lr0, double lr_min, uint64_t halving, double b1,
+                  double b2, cudaStream_t s);
 void adam_flat(float* p, float* m, float* v, const float* g, uint64_t n, const StepDev* sd,
                float b1, float b2, float eps, __nv_bfloat16* shadow, uint64_t sh_begin, uint64_t sh_end,
                cudaStream_t s);

@@ -85,6 +85,7 @@ struct mel_ctx {
   // stream overlapped with the rest of the backward, Adam on this rank's W_L row
   // shard, all-gather of the bf16 shadow
   bool zero = false;
+  bool fused_adam = false;                  // world == 1, bf16: Adam of W_L inside K1
   uint64_t shard_elems = 0, shard_off = 0;   // W_L elements per rank, this rank's offset in W_L
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_gw = nullptr, ev_head = nullptr, ev_ar = nullptr, ev_adam = nullptr, ev_ag = nullptr;
@@ -404,7 +405,19 @@ int train_step_bf16(mel_ctx* c) {
   }
   tc::OutTcArgs a{};
   a.N = c->N; a.Npad = c->Npad; a.B = B; a.K = K;
+  a.shadow_idx = c->shadow_cur;
   a.w_bf16 = c->d_shadow[c->shadow_cur];
+  a.fused_adam = c->fused_adam ? 1 : 0;
+  if (c->fused_adam) {
+    const uint64_t offW = c->off[2 * (L - 1)];
+    a.adam_p = c->d_p + offW; a.adam_m = c->d_m + offW; a.adam_v = c->d_v + offW;
+    a.shadow_out = c->d_shadow[c->shadow_cur ^ 1];
+    a.sd = c->d_sd;
+    a.b1 = (float)c->cfg.beta1; a.b2 = (float)c->cfg.beta2; a.eps = (float)c->cfg.eps;
+    Timer t(c, MEL_K_LOSS, 1);
+    step_prepare(c->d_sd, c->d_st, (double)c->N, c->cfg.lr0, c->cfg.lr_min, c->cfg.lr_halving_samples,
+                 c->cfg.beta1, c->cfg.beta2, c->stream);
+  }
   a.b = c->d_p + c->off[2 * (L - 1) + 1];
   a.h_bf16 = c->tcb.h_bf16;
   a.payload = static_cast<const __nv_bfloat16*>(c->ra.payload);
@@ -570,6 +583,7 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
     DALLOC(c->d_sse_part, c->max_parts);
   } else {
     DALLOC(c->d_shadow[0], (size_t)c->Npad * c->Klast);
+    DALLOC(c->d_shadow[1], (size_t)c->Npad * c->Klast);
     r = tc::alloc_buffers(c->tcb, c->Npad, c->B, c->Klast);
     if (r) return fail(c, MEL_ENOMEM, "tensor-core scratch allocation failed");
     c->part_elems = tc::dh_part_elems(c->B, c->Klast);
@@ -578,7 +592,8 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
     c->max_parts = tc::max_sse_parts(c->Npad);
     DALLOC(c->d_sse_part, c->max_parts);
     to_bf16(c->d_p + c->off[2 * (c->L - 1)], c->d_shadow[0], c->Npad * c->Klast, c->stream);
-    r = tc::prepare(c->tcb, c->Npad, c->B, c->Klast, c->d_shadow[0],
+    const __nv_bfloat16* shadows[2] = {c->d_shadow[0], c->d_shadow[1]};
+    r = tc::prepare(c->tcb, c->Npad, c->B, c->Klast, shadows,
                     static_cast<const __nv_bfloat16*>(c->ra.payload), c->C, c->d_g + c->off[2 * (c->L - 1)]);
     if (r) return fail(c, MEL_ECUDA, "tensor-core kernel setup failed: %s", tc::last_error());
   }
@@ -586,6 +601,7 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
   if (r) return r;
   CK(cudaStreamSynchronize(c->stream));
 
+  c->fused_adam = (c->world == 1) && (g->precision == MEL_BF16) && (g->flags & MEL_FLAG_FUSED_ADAM);
   if (c->world > 1) {
     ncclUniqueId id;
     memcpy(&id, nccl_id, sizeof id);
@@ -835,7 +851,13 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
     step_finalize(c->d_sd, (double)c->N, c->cfg.lr0, c->cfg.lr_min, c->cfg.lr_halving_samples, c->cfg.beta1,
                   c->cfg.beta2, c->d_mirror, c->d_st, c->stream);
   }
-  if (c->zero) {
+  if (c->fused_adam) {
+    // W_L was updated inside K1 (new shadow in the other buffer); the small region here
+    Timer t(c, MEL_K_ADAM, 1);
+    adam_flat(c->d_p, c->d_m, c->d_v, c->d_g, c->off[2 * (c->L - 1)], c->d_sd, (float)c->cfg.beta1,
+              (float)c->cfg.beta2, (float)c->cfg.eps, nullptr, 0, 0, c->stream);
+    c->shadow_cur ^= 1;
+  } else if (c->zero) {
     // small region (head weights, every bias) replicated; W_L on this rank's row shard,
     // refreshing the shard of the bf16 shadow, then all-gather of the shadow
     Timer t(c, MEL_K_ADAM, 2);
@@ -843,7 +865,7 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
     const float b1 = (float)c->cfg.beta1, b2 = (float)c->cfg.beta2, eps = (float)c->cfg.eps;
     adam_flat(c->d_p, c->d_m, c->d_v, c->d_g, offW, c->d_sd, b1, b2, eps, nullptr, 0, 0, c->stream);
     adam_flat(c->d_p + so, c->d_m + so, c->d_v + so, c->d_g + so, c->shard_elems, c->d_sd, b1, b2, eps,
-              c->d_shadow[0] + c->shard_off, 0, c->shard_elems, c->stream);
+              c->d_shadow[c->shadow_cur] + c->shard_off, 0, c->shard_elems, c->stream);
   } else {
     Timer t(c, MEL_K_ADAM, 1);
     __nv_bfloat16* sh = nullptr;
@@ -851,7 +873,7 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
     if (c->cfg.precision == MEL_BF16) {
       // the output-layer kernels of this step have completed (stream order), so
       // the bf16 shadow is refreshed in place from the updated fp32 master
-      sh = c->d_shadow[0];
+      sh = c->d_shadow[c->shadow_cur];
       b0 = c->off[2 * (c->L - 1)];
       b1 = b0 + c->Npad * c->Klast;
     }
@@ -862,7 +884,7 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
     Timer t(c, MEL_K_ALLREDUCE, 0, c->comm_stream);
     CK(cudaEventRecord(c->ev_adam, c->stream));
     CK(cudaStreamWaitEvent(c->comm_stream, c->ev_adam, 0));
-    if ((r = gather_shards(c, c->d_shadow[0], 2, ncclBfloat16))) return r;
+    if ((r = gather_shards(c, c->d_shadow[c->shadow_cur], 2, ncclBfloat16))) return r;
     CK(cudaEventRecord(c->ev_ag, c->comm_stream));
     c->ag_pending = true;
   }

@@ -235,6 +235,20 @@ __global__ void step_finalize_kernel(StepDev* sd, double n_field, double lr0, do
   mirror->adam_k = k; mirror->samples = sd->S;
 }
 
+// Step scalars ahead of the output-layer kernel (world == 1, fused Adam): the same
+// values step_finalize computes afterwards (scale, lr, bias corrections of step k+1).
+__global__ void step_prepare_kernel(StepDev* sd, const ResDev* st, double n_field, double lr0, double lr_min,
+                                    uint64_t halving, double b1, double b2) {
+  const double n = (double)st->n_last;
+  if (n <= 0.0) { sd->skip = 1; return; }
+  sd->skip = 0;
+  sd->scale = (float)(1.0 / (n_field * n));
+  sd->lr = (float)fmax(lr_min, lr0 * exp2(-(double)(sd->S / halving)));
+  const uint64_t k = sd->k + 1;
+  sd->c1 = (float)(1.0 - pow(b1, (double)k));
+  sd->c2 = (float)(1.0 - pow(b2, (double)k));
+}
+
 // Adam (bias-corrected), flat over every tensor; g is the raw dS/dtheta and is
 // scaled by 1/(N * n_total) here.  Writes the bf16 shadow of [sh_begin, sh_end).
 // Two float4 per array in flight per thread (memory-level parallelism).
@@ -404,6 +418,11 @@ void reduce_local(StepDev* sd, const double* parts, int n_parts, const ResDev* s
 void step_finalize(StepDev* sd, double n_field, double lr0, double lr_min, uint64_t halving, double b1, double b2,
                    Mirror* mirror, ResDev* st, cudaStream_t s) {
   step_finalize_kernel<<<1, 1, 0, s>>>(sd, n_field, lr0, lr_min, halving, b1, b2, mirror, st);
+}
+
+void step_prepare(StepDev* sd, const ResDev* st, double n_field, double lr0, double lr_min, uint64_t halving, double b1,
+                  double b2, cudaStream_t s) {
+  step_prepare_kernel<<<1, 1, 0, s>>>(sd, st, n_field, lr0, lr_min, halving, b1, b2);
 }
 
 void adam_flat(float* p, float* m, float* v, const float* g, uint64_t n, const StepDev* sd, float b1, float b2,

@@ -37,11 +37,17 @@ struct OutTcArgs {
   float* dh_part;                    // scratch: split-K partials of dS/dH
   float* dz;                         // out: dS/dZ_{L-1} [B][K]
   const float* z;                    // Z_{L-1} [B][K] (ReLU mask)
+  int shadow_idx;                    // which ping-pong W_L shadow K1 and K2 read
+  int fused_adam;                    // K1 applies Adam to W_L (world == 1)
+  float *adam_p, *adam_m, *adam_v;   // W_L fp32 master / moments (fused)
+  __nv_bfloat16* shadow_out;         // updated bf16 shadow (fused), the other buffer
+  const StepDev* sd;                 // step scalars (scale, lr, bias corrections, skip)
+  float b1, b2, eps;
 };
 
 int alloc_buffers(TcBuffers& t, uint64_t Npad, uint32_t B, uint32_t K);
 void free_buffers(TcBuffers& t);
-int prepare(TcBuffers& t, uint64_t Npad, uint32_t B, uint32_t K, const __nv_bfloat16* w_bf16,
+int prepare(TcBuffers& t, uint64_t Npad, uint32_t B, uint32_t K, const __nv_bfloat16* const* w_bf16,
             const __nv_bfloat16* payload, uint32_t capacity, const float* grad_w);   // TMA descriptors, kernel attributes
 size_t dh_part_elems(uint32_t B, uint32_t K);
 int max_sse_parts(uint64_t Npad);

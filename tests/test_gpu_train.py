@@ -25,15 +25,16 @@ def _bf16_wl(**kw):
     return replace(base, **kw)
 
 
-@pytest.mark.parametrize("n,batch", [(100, 256), (37, 64), (101, 192)], ids=["N1e4-B256", "N1369-B64", "N10201-B192"])
-def test_bf16_step_reanchored(mel, n, batch):
+@pytest.mark.parametrize("n,batch,flags", [(100, 256, 0), (37, 64, 0), (101, 192, 0), (100, 256, 4)],
+                         ids=["N1e4-B256", "N1369-B64", "N10201-B192", "N1e4-B256-fusedAdam"])
+def test_bf16_step_reanchored(mel, n, batch, flags):
     """One re-anchored bf16 step at a time: the GPU's output layer runs on
     tcgen05 with bf16 operands (W shadow, H, dY) and fp32 TMEM accumulation.
     Sizes span several 128-row tiles, ragged tails (N % 128 != 0) and B not a
     multiple of 128."""
     wl = _bf16_wl(n=n, batch=batch, hidden=(256, 256))
     table = FieldTable(wl)
-    ctx = mel.Context(make_config(wl, precision=1, storage=1))
+    ctx = mel.Context(make_config(wl, precision=1, storage=1, flags=flags))
     rep = replay_parity(ctx, wl, table, design.build_oplog(wl), storage=1, max_train_steps=6)
     print("bf16 re-anchored: loss err %.3e  weight err %.3e" % (max(rep["loss_err"]), max(rep["w_err"])))
     assert rep["steps"] == 6
