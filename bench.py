@@ -288,7 +288,7 @@ def main():
         if rank == 0:
             prof = ctx.debug_counters().reshape(160, 32)[:148].astype(np.float64)
             names = {0: "mma_total", 1: "mma_w_full", 2: "mma_h_full", 3: "mma_y_empty", 4: "mma_dy_full",
-                     5: "mma_dw_empty", 8: "epi_total", 9: "epi_t_full", 10: "epi_y_full", 11: "epi_dy_empty",
+                     5: "mma_dw_empty", 6: "mma_fwd_issue", 7: "mma_dw_issue", 8: "epi_total", 9: "epi_t_full", 10: "epi_y_full", 11: "epi_dy_empty",
                      12: "epi_store_bar", 13: "epi_dw_readout", 14: "epi_db_bar", 16: "tma_total", 17: "tma_w_empty",
                      18: "tma_h_empty", 24: "ld_total", 25: "ld_t_empty"}
             k1 = {v: float(prof[:, k].mean()) for k, v in names.items()}

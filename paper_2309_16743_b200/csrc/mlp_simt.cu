@@ -276,6 +276,17 @@ __device__ __forceinline__ void store_shadow(__nv_bfloat16* shadow, uint64_t e, 
   }
 }
 
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(float4* p, const float4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+
+// UNR float4 of each array in flight per thread; the tail loop handles the rest
+template <int UNR>
 __global__ void __launch_bounds__(256)
 adam_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v, const float* __restrict__ g,
             uint64_t n4, const StepDev* __restrict__ sd, float b1, float b2, float eps,
@@ -288,17 +299,22 @@ adam_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
   float4* V4 = reinterpret_cast<float4*>(v);
   const float4* G4 = reinterpret_cast<const float4*>(g);
   uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  for (; i + stride < n4; i += 2 * stride) {
-    const uint64_t j = i + stride;
-    float4 pa = P4[i], pb = P4[j], ma = M4[i], mb = M4[j], va = V4[i], vb = V4[j];
-    const float4 ga = __ldcs(G4 + i), gb = __ldcs(G4 + j);
-    adam4(pa, ma, va, ga, scale, step, isc2, b1, b2, eps);
-    adam4(pb, mb, vb, gb, scale, step, isc2, b1, b2, eps);
-    P4[i] = pa; P4[j] = pb; M4[i] = ma; M4[j] = mb; V4[i] = va; V4[j] = vb;
-    store_shadow(shadow, 4 * i, sh_begin, sh_end, pa);
-    store_shadow(shadow, 4 * j, sh_begin, sh_end, pb);
+  for (; i + (UNR - 1) * stride < n4; i += UNR * stride) {
+    float4 pa[UNR], ma[UNR], va[UNR], ga[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const uint64_t j = i + u * stride;
+      pa[u] = P4[j]; ma[u] = M4[j]; va[u] = V4[j]; ga[u] = __ldcs(G4 + j);
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const uint64_t j = i + u * stride;
+      adam4(pa[u], ma[u], va[u], ga[u], scale, step, isc2, b1, b2, eps);
+      P4[j] = pa[u]; M4[j] = ma[u]; V4[j] = va[u];
+      store_shadow(shadow, 4 * j, sh_begin, sh_end, pa[u]);
+    }
   }
-  if (i < n4) {
+  for (; i < n4; i += stride) {
     float4 pa = P4[i], ma = M4[i], va = V4[i];
     const float4 ga = G4[i];
     adam4(pa, ma, va, ga, scale, step, isc2, b1, b2, eps);
@@ -428,7 +444,7 @@ void step_prepare(StepDev* sd, const ResDev* st, double n_field, double lr0, dou
 void adam_flat(float* p, float* m, float* v, const float* g, uint64_t n, const StepDev* sd, float b1, float b2,
                float eps, __nv_bfloat16* shadow, uint64_t sh_begin, uint64_t sh_end, cudaStream_t s) {
   const uint64_t n4 = n / 4;   // the flat buffer is padded to a multiple of 4
-  adam_kernel<<<grid_for(n4, 256, 148 * 16), 256, 0, s>>>(p, m, v, g, n4, sd, b1, b2, eps, shadow, sh_begin, sh_end);
+  adam_kernel<2><<<grid_for(n4, 256, 148 * 16), 256, 0, s>>>(p, m, v, g, n4, sd, b1, b2, eps, shadow, sh_begin, sh_end);
 }
 
 void init_tensor(float* dst, uint64_t count, uint32_t tid, uint32_t fan_in, uint64_t seed, cudaStream_t s) {
