@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--grid", type=int, default=N_GRID)
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--profile", action="store_true", help="timed region only (for ncu)")
+    ap.add_argument("--flags", type=int, default=0, help="MEL_FLAG_* bits (e.g. 4 = fused Adam)")
     return ap.parse_args()
 
 
@@ -201,7 +202,7 @@ def main():
     n_field = args.grid * args.grid
     B, k = args.batch, args.puts_per_step
     cfg = mel.Config(n_field=n_field, hidden=HIDDEN, capacity=CAP, threshold=THETA, batch=B, steps_per_sim=TAU,
-                     precision=mel.BF16, storage=mel.STORE_BF16, seed=1, staging_entries=32)
+                     precision=mel.BF16, storage=mel.STORE_BF16, seed=1, staging_entries=32, flags=args.flags)
     # a dedicated stream shared by torch (events, data generation) and libmel, so
     # that CUDA events bracket exactly the library's work
     stream = torch.cuda.Stream(dev)
@@ -295,7 +296,7 @@ def main():
             print(json.dumps({"ms_per_step": ms_step, "value": value, "k1_wait_cycles_mean_per_cta": k1}), flush=True)
         return 0
     # ---- per-kernel timing pass (CUDA events around each kernel class) ----
-    ctx.set_flags(mel.FLAG_TIMING)
+    ctx.set_flags(mel.FLAG_TIMING | args.flags)
     ctx.kernel_time_reset()
     n_kt = min(args.steps, 10)
     extra = [next_batch(k) for _ in range(n_kt)]
@@ -315,7 +316,7 @@ def main():
     for kid, name in enumerate(mel.KERNEL_NAMES):
         tms, nl = ctx.kernel_time(kid)
         kernels[name] = {"ms_per_step": tms / n_kt, "share": tms / kt_total if kt_total else None}
-    ctx.set_flags(0)
+    ctx.set_flags(args.flags)
     P = peaks()
     K = HIDDEN[-1]
     n_params = ctx.n_params
