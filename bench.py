@@ -337,7 +337,8 @@ def main():
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        traffic = prof.get(dom, {}).get("dram_bytes_per_launch")
+        ent = prof.get(dom) or prof.get(dom + "_kernel") or {}
+        traffic = ent.get("dram_bytes_per_launch")
     except Exception:
         pass
     roofline = {"kernel": dom, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit_r,
