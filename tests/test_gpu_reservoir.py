@@ -123,3 +123,16 @@ def test_device_resident_puts_match_host_puts(mel):
     da, db = a.dump(), b.dump()
     for k in da:
         assert np.array_equal(da[k], db[k]), k
+
+
+def test_degenerate_capacity_one_threshold_zero(mel):
+    """C = 1, theta = 0, B = 1: every put after the first must wait for the single
+    item to be seen, and each commit evicts it; trained to EOS."""
+    wl = replace(design.TINY, capacity=1, threshold=0, batch=1, puts_per_step=2, sims=4)
+    table = FieldTable(wl)
+    ctx = mel.Context(make_config(wl, staging=64))   # back-pressure keeps up to 40 puts pending
+    rep = replay_parity(ctx, wl, table, design.build_oplog(wl, n_steps_after_close=60))
+    res = rep["oracle_res"]
+    compare_reservoir(ctx, res)
+    assert res.evictions > 0 and rep["steps"] > 10
+    assert max(rep["loss_err"]) <= 1e-5 and max(rep["w_err"]) <= 1e-5

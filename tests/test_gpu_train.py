@@ -92,3 +92,37 @@ def test_eval_matches_oracle(mel, precision):
     assert abs(mse - want) / want < 1e-5
     Y = mlp.forward(params, xn)[1][-1] * 400.0 + 100.0
     assert np.max(np.abs(pred - Y)) < 1e-2
+
+
+def test_bf16_to_eos_with_short_drain_batches(mel):
+    """bf16 path through reception, close and drain (batches shorter than B, then
+    EOS); hidden 64x64 exercises the K = 64 instantiation of the tensor-core kernels."""
+    wl = replace(design.MEDIUM, name="bf16-eos", n=16, tau=10, sims=12, hidden=(64, 64), capacity=48, threshold=8,
+                 batch=64, puts_per_step=20)
+    table = FieldTable(wl)
+    ctx = mel.Context(make_config(wl, precision=1, storage=1))
+    rep = replay_parity(ctx, wl, table, design.build_oplog(wl), storage=1)
+    res = rep["oracle_res"]
+    assert res.over and res.p == 0
+    assert rep["samples"] % wl.batch != 0            # at least one short drain batch
+    assert max(rep["loss_err"]) <= 2e-2 and max(rep["w_err"]) <= 1e-3, (max(rep["loss_err"]), max(rep["w_err"]))
+
+
+@pytest.mark.parametrize("hidden,batch", [((128,), 128), ((256, 256), 2048)], ids=["one-hidden-K128", "B2048"])
+def test_bf16_shapes(mel, hidden, batch):
+    wl = _bf16_wl(n=64, batch=batch, hidden=hidden, capacity=4096, threshold=2048, sims=80, puts_per_step=1000)
+    table = FieldTable(wl)
+    ctx = mel.Context(make_config(wl, precision=1, storage=1))
+    rep = replay_parity(ctx, wl, table, design.build_oplog(wl), storage=1, max_train_steps=3)
+    assert rep["steps"] == 3
+    assert max(rep["loss_err"]) <= 2e-2 and max(rep["w_err"]) <= 1e-3, (max(rep["loss_err"]), max(rep["w_err"]))
+
+
+def test_invalid_configurations_fail_loudly(mel):
+    base = dict(n_field=400, hidden=(256, 256), capacity=100, threshold=10, batch=128, precision=1, storage=1)
+    for bad in (dict(threshold=100), dict(batch=0), dict(batch=96), dict(hidden=(256, 100)), dict(storage=0),
+                dict(n_field=0)):
+        cfg = mel.Config(**{**base, **bad})
+        with pytest.raises(mel.MelError) as e:
+            mel.Context(cfg)
+        assert e.value.code == mel.EINVAL
