@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -90,6 +91,13 @@ struct mel_ctx {
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_gw = nullptr, ev_head = nullptr, ev_ar = nullptr, ev_adam = nullptr, ev_ag = nullptr;
   bool ag_pending = false;
+  // bucketed pipeline: K1 runs over NB tile ranges; bucket j's dW_L reduce-scatter overlaps
+  // K1 of bucket j+1, and the next step's K1 bucket j waits only for its shadow all-gather
+  static constexpr int NBMAX = 8;
+  int nb = 1;
+  uint32_t bt0[NBMAX] = {}, bt1[NBMAX] = {};
+  cudaEvent_t ev_k1[NBMAX] = {}, ev_agb[NBMAX] = {};
+  int sm_reserve = 0;
 
   // timing
   std::vector<TimedPair> pending;
@@ -267,9 +275,6 @@ int world_exchange(mel_ctx* c) {
   CK(cudaEventRecord(c->ev_head, c->stream));
   {
     Timer t(c, MEL_K_ALLREDUCE, 0, c->comm_stream);
-    CK(cudaStreamWaitEvent(c->comm_stream, c->ev_gw, 0));
-    float* gW = c->d_g + offW;
-    NK(ncclReduceScatter(gW, gW + c->shard_off, c->shard_elems, ncclFloat32, ncclSum, c->comm, c->comm_stream));
     CK(cudaStreamWaitEvent(c->comm_stream, c->ev_head, 0));
     NK(ncclGroupStart());
     NK(ncclAllReduce(c->d_g, c->d_g, offW, ncclFloat32, ncclSum, c->comm, c->comm_stream));
@@ -281,17 +286,32 @@ int world_exchange(mel_ctx* c) {
   return MEL_OK;
 }
 
-// all-gather of a W_L-shaped buffer from the row shards (collective, comm stream)
+// bucket j of W_L: rows [128 bt0, 128 bt1); this rank owns the r-th of R equal parts
+inline uint64_t bucket_row0(const mel_ctx* c, int j) { return (uint64_t)c->bt0[j] * 128; }
+inline uint64_t bucket_rows(const mel_ctx* c, int j) { return (uint64_t)(c->bt1[j] - c->bt0[j]) * 128; }
+inline uint64_t part_elems(const mel_ctx* c, int j) { return bucket_rows(c, j) / c->world * c->Klast; }
+inline uint64_t part_off(const mel_ctx* c, int j) {   // elements from the start of W_L
+  return bucket_row0(c, j) * c->Klast + (uint64_t)c->rank * part_elems(c, j);
+}
+
+// all-gather of one bucket of a W_L-shaped buffer from the rank parts (comm stream)
+int gather_bucket(mel_ctx* c, void* base, size_t esz, ncclDataType_t ty, int j) {
+  char* b = static_cast<char*>(base) + bucket_row0(c, j) * c->Klast * esz;
+  NK(ncclAllGather(b + (uint64_t)c->rank * part_elems(c, j) * esz, b, part_elems(c, j), ty, c->comm, c->comm_stream));
+  return MEL_OK;
+}
 int gather_shards(mel_ctx* c, void* base, size_t esz, ncclDataType_t ty) {
-  char* b = static_cast<char*>(base);
-  NK(ncclAllGather(b + c->shard_off * esz, b, c->shard_elems, ty, c->comm, c->comm_stream));
+  for (int j = 0; j < c->nb; ++j) {
+    int r = gather_bucket(c, base, esz, ty, j);
+    if (r) return r;
+  }
   return MEL_OK;
 }
 
 // wait (device-side) for the pending shadow all-gather before anything reads W_L
 int wait_shadow(mel_ctx* c) {
   if (c->ag_pending) {
-    CK(cudaStreamWaitEvent(c->stream, c->ev_ag, 0));
+    for (int j = 0; j < c->nb; ++j) CK(cudaStreamWaitEvent(c->stream, c->ev_agb[j], 0));
     c->ag_pending = false;
   }
   return MEL_OK;
@@ -430,13 +450,28 @@ int train_step_bf16(mel_ctx* c) {
   a.dz = c->d_dz[L - 2];
   a.z = c->d_z[L - 2];
   int nparts = 0;
-  int r0 = wait_shadow(c);
-  if (r0) return r0;
-  {
+  if (!c->zero) {
+    int r0 = wait_shadow(c);
+    if (r0) return r0;
     Timer t(c, MEL_K_OUT_FWD_DW, 1);
     nparts = tc::launch_out_fwd_dw(a, c->tcb, c->stream);
+  } else {
+    float* gW = c->d_g + c->off[2 * (L - 1)];
+    for (int j = 0; j < c->nb; ++j) {
+      if (c->ag_pending) CK(cudaStreamWaitEvent(c->stream, c->ev_agb[j], 0));   // this bucket's shadow rows
+      {
+        Timer t(c, MEL_K_OUT_FWD_DW, 1);
+        nparts += tc::launch_out_fwd_dw(a, c->tcb, c->stream, c->bt0[j], c->bt1[j], (uint32_t)nparts);
+      }
+      CK(cudaEventRecord(c->ev_k1[j], c->stream));
+      Timer t(c, MEL_K_ALLREDUCE, 0, c->comm_stream);
+      CK(cudaStreamWaitEvent(c->comm_stream, c->ev_k1[j], 0));
+      float* gb = gW + bucket_row0(c, j) * K;
+      NK(ncclReduceScatter(gb, gb + (uint64_t)c->rank * part_elems(c, j), part_elems(c, j), ncclFloat32, ncclSum,
+                           c->comm, c->comm_stream));
+    }
+    c->ag_pending = false;
   }
-  if (c->zero) CK(cudaEventRecord(c->ev_gw, c->stream));
   {
     Timer t(c, MEL_K_OUT_DH, 2);
     tc::launch_out_dh(a, c->tcb, c->stream);
@@ -593,8 +628,24 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
     DALLOC(c->d_sse_part, c->max_parts);
     to_bf16(c->d_p + c->off[2 * (c->L - 1)], c->d_shadow[0], c->Npad * c->Klast, c->stream);
     const __nv_bfloat16* shadows[2] = {c->d_shadow[0], c->d_shadow[1]};
+    c->zero = (c->world > 1) && !(g->flags & MEL_FLAG_NO_ZERO);
+    // tuning knobs for the overlapped exchange (environment, diagnostics only)
+    const char* e_res = getenv("MEL_SM_RESERVE");
+    const char* e_nb = getenv("MEL_BUCKETS");
+    c->sm_reserve = c->zero ? (e_res ? atoi(e_res) : 0) : 0;
+    if (c->zero) {
+      const uint32_t tiles = (uint32_t)(c->Npad / 128);
+      c->nb = tiles >= 64 ? (e_nb ? atoi(e_nb) : 1) : 1;
+      if (c->nb < 1) c->nb = 1;
+      if (c->nb > mel_ctx::NBMAX) c->nb = mel_ctx::NBMAX;
+      for (int j = 0; j < c->nb; ++j) {
+        c->bt0[j] = (uint32_t)((uint64_t)tiles * j / c->nb);
+        c->bt1[j] = (uint32_t)((uint64_t)tiles * (j + 1) / c->nb);
+      }
+    }
     r = tc::prepare(c->tcb, c->Npad, c->B, c->Klast, shadows,
-                    static_cast<const __nv_bfloat16*>(c->ra.payload), c->C, c->d_g + c->off[2 * (c->L - 1)]);
+                    static_cast<const __nv_bfloat16*>(c->ra.payload), c->C, c->d_g + c->off[2 * (c->L - 1)],
+                    c->sm_reserve);
     if (r) return fail(c, MEL_ECUDA, "tensor-core kernel setup failed: %s", tc::last_error());
   }
   r = check_launch(c, "create");
@@ -605,13 +656,18 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
   if (c->world > 1) {
     ncclUniqueId id;
     memcpy(&id, nccl_id, sizeof id);
-    NK(ncclCommInitRank(&c->comm, c->world, id, c->rank));
-    c->zero = (g->precision == MEL_BF16) && !(g->flags & MEL_FLAG_NO_ZERO);
+    ncclConfig_t ncfg = NCCL_CONFIG_INITIALIZER;
+    if (c->zero && c->sm_reserve > 0) ncfg.maxCTAs = c->sm_reserve;   // NCCL on the SMs the kernels leave free
+    NK(ncclCommInitRankConfig(&c->comm, c->world, id, c->rank, &ncfg));
     c->shard_elems = c->Npad / c->world * c->Klast;
     c->shard_off = (uint64_t)c->rank * c->shard_elems;
     CK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
     cudaEvent_t* evs[] = {&c->ev_gw, &c->ev_head, &c->ev_ar, &c->ev_adam, &c->ev_ag};
     for (cudaEvent_t* e : evs) CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    for (int j = 0; j < c->nb; ++j) {
+      CK(cudaEventCreateWithFlags(&c->ev_k1[j], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_agb[j], cudaEventDisableTiming));
+    }
   }
   return MEL_OK;
 }
@@ -643,6 +699,10 @@ void mel_destroy(mel_ctx* c) {
   cudaEvent_t evs[] = {c->ev_gw, c->ev_head, c->ev_ar, c->ev_adam, c->ev_ag};
   for (cudaEvent_t e : evs)
     if (e) cudaEventDestroy(e);
+  for (int j = 0; j < mel_ctx::NBMAX; ++j) {
+    if (c->ev_k1[j]) cudaEventDestroy(c->ev_k1[j]);
+    if (c->ev_agb[j]) cudaEventDestroy(c->ev_agb[j]);
+  }
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   drain_timers(c);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -860,12 +920,15 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
   } else if (c->zero) {
     // small region (head weights, every bias) replicated; W_L on this rank's row shard,
     // refreshing the shard of the bf16 shadow, then all-gather of the shadow
-    Timer t(c, MEL_K_ADAM, 2);
-    const uint64_t offW = c->off[2 * (c->L - 1)], so = offW + c->shard_off;
+    Timer t(c, MEL_K_ADAM, 1 + c->nb);
+    const uint64_t offW = c->off[2 * (c->L - 1)];
     const float b1 = (float)c->cfg.beta1, b2 = (float)c->cfg.beta2, eps = (float)c->cfg.eps;
     adam_flat(c->d_p, c->d_m, c->d_v, c->d_g, offW, c->d_sd, b1, b2, eps, nullptr, 0, 0, c->stream);
-    adam_flat(c->d_p + so, c->d_m + so, c->d_v + so, c->d_g + so, c->shard_elems, c->d_sd, b1, b2, eps,
-              c->d_shadow[c->shadow_cur] + c->shard_off, 0, c->shard_elems, c->stream);
+    for (int j = 0; j < c->nb; ++j) {
+      const uint64_t po = part_off(c, j), so = offW + po, n = part_elems(c, j);
+      adam_flat(c->d_p + so, c->d_m + so, c->d_v + so, c->d_g + so, n, c->d_sd, b1, b2, eps,
+                c->d_shadow[c->shadow_cur] + po, 0, n, c->stream);
+    }
   } else {
     Timer t(c, MEL_K_ADAM, 1);
     __nv_bfloat16* sh = nullptr;
@@ -884,8 +947,10 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
     Timer t(c, MEL_K_ALLREDUCE, 0, c->comm_stream);
     CK(cudaEventRecord(c->ev_adam, c->stream));
     CK(cudaStreamWaitEvent(c->comm_stream, c->ev_adam, 0));
-    if ((r = gather_shards(c, c->d_shadow[c->shadow_cur], 2, ncclBfloat16))) return r;
-    CK(cudaEventRecord(c->ev_ag, c->comm_stream));
+    for (int j = 0; j < c->nb; ++j) {
+      if ((r = gather_bucket(c, c->d_shadow[c->shadow_cur], 2, ncclBfloat16, j))) return r;
+      CK(cudaEventRecord(c->ev_agb[j], c->comm_stream));
+    }
     c->ag_pending = true;
   }
   if ((r = check_launch(c, "adam"))) return r;

@@ -48,11 +48,12 @@ struct OutTcArgs {
 int alloc_buffers(TcBuffers& t, uint64_t Npad, uint32_t B, uint32_t K);
 void free_buffers(TcBuffers& t);
 int prepare(TcBuffers& t, uint64_t Npad, uint32_t B, uint32_t K, const __nv_bfloat16* const* w_bf16,
-            const __nv_bfloat16* payload, uint32_t capacity, const float* grad_w);   // TMA descriptors, kernel attributes
+            const __nv_bfloat16* payload, uint32_t capacity, const float* grad_w, int sm_reserve);   // TMA descriptors, kernel attributes
 size_t dh_part_elems(uint32_t B, uint32_t K);
 int max_sse_parts(uint64_t Npad);
 // forward + MSE gradient + dW_L/db_L (per 128-row tile of W_L); returns #SSE partials
-int launch_out_fwd_dw(const OutTcArgs& a, const TcBuffers& t, cudaStream_t s);
+int launch_out_fwd_dw(const OutTcArgs& a, const TcBuffers& t, cudaStream_t s, uint32_t tile0 = 0, uint32_t tile1 = 0,
+                      uint32_t part_base = 0);
 // dS/dH = dY W_L (split-K over N) then the ReLU' mask -> dz
 void launch_out_dh(const OutTcArgs& a, const TcBuffers& t, cudaStream_t s);
 const char* last_error();
