@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--grid", type=int, default=N_GRID)
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--profile", action="store_true", help="timed region only (for ncu)")
-    ap.add_argument("--flags", type=int, default=0, help="MEL_FLAG_* bits (e.g. 4 = fused Adam)")
+    ap.add_argument("--flags", type=int, default=0, help="MEL_FLAG_* bits (e.g. 8 = Adam of W_L as a separate kernel)")
     return ap.parse_args()
 
 
@@ -287,7 +287,8 @@ def main():
 
     if args.profile:
         if rank == 0:
-            prof = ctx.debug_counters().reshape(160, 32)[:148].astype(np.float64)
+            raw = ctx.debug_counters().reshape(160, 32)
+            prof = raw[:148].astype(np.float64)
             names = {0: "mma_total", 1: "mma_w_full", 2: "mma_h_full", 3: "mma_y_empty", 4: "mma_dy_full",
                      5: "mma_dw_empty", 6: "mma_fwd_issue", 7: "mma_dw_issue", 8: "epi_total", 9: "epi_t_full", 10: "epi_y_full", 11: "epi_dy_empty",
                      12: "epi_store_bar", 13: "epi_dw_readout", 14: "epi_db_bar", 16: "tma_total", 17: "tma_w_empty",

@@ -95,9 +95,10 @@ typedef struct {
 } mel_config;
 
 #define MEL_FLAG_TIMING 1u     /* record CUDA events around every kernel (bench roofline) */
-#define MEL_FLAG_FUSED_ADAM 4u /* world == 1, bf16: Adam of W_L inside the output-layer kernel's
-                                  dW epilogue (saves the gradient round trip; slower today: the
-                                  Adam traffic serialises with the MMA pipeline)   */
+#define MEL_FLAG_UNFUSED_ADAM 8u /* world == 1, bf16: run Adam of W_L as its own kernel over a
+                                    stored gradient instead of inside the output-layer kernel's
+                                    dW epilogue (the default there).  Read at
+                                    mel_create only.                                        */
 #define MEL_FLAG_NO_ZERO 2u    /* world > 1, bf16: plain all-reduce + replicated Adam instead of
                                   reduce-scatter / sharded Adam / shadow all-gather            */
 

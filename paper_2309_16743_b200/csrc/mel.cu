@@ -645,14 +645,15 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
     }
     r = tc::prepare(c->tcb, c->Npad, c->B, c->Klast, shadows,
                     static_cast<const __nv_bfloat16*>(c->ra.payload), c->C, c->d_g + c->off[2 * (c->L - 1)],
-                    c->sm_reserve);
+                    c->sm_reserve, c->d_p + c->off[2 * (c->L - 1)], c->d_m + c->off[2 * (c->L - 1)],
+                    c->d_v + c->off[2 * (c->L - 1)]);
     if (r) return fail(c, MEL_ECUDA, "tensor-core kernel setup failed: %s", tc::last_error());
   }
   r = check_launch(c, "create");
   if (r) return r;
   CK(cudaStreamSynchronize(c->stream));
 
-  c->fused_adam = (c->world == 1) && (g->precision == MEL_BF16) && (g->flags & MEL_FLAG_FUSED_ADAM);
+  c->fused_adam = (c->world == 1) && (g->precision == MEL_BF16) && !(g->flags & MEL_FLAG_UNFUSED_ADAM);
   if (c->world > 1) {
     ncclUniqueId id;
     memcpy(&id, nccl_id, sizeof id);

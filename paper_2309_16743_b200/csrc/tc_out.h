@@ -48,7 +48,8 @@ struct OutTcArgs {
 int alloc_buffers(TcBuffers& t, uint64_t Npad, uint32_t B, uint32_t K);
 void free_buffers(TcBuffers& t);
 int prepare(TcBuffers& t, uint64_t Npad, uint32_t B, uint32_t K, const __nv_bfloat16* const* w_bf16,
-            const __nv_bfloat16* payload, uint32_t capacity, const float* grad_w, int sm_reserve);   // TMA descriptors, kernel attributes
+            const __nv_bfloat16* payload, uint32_t capacity, const float* grad_w, int sm_reserve,
+            const float* p_w, const float* m_w, const float* v_w);   // TMA descriptors, kernel attributes
 size_t dh_part_elems(uint32_t B, uint32_t K);
 int max_sse_parts(uint64_t Npad);
 // forward + MSE gradient + dW_L/db_L (per 128-row tile of W_L); returns #SSE partials

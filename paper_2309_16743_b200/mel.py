@@ -19,7 +19,7 @@ FP32, BF16 = 0, 1
 STORE_F32, STORE_BF16 = 0, 1
 FLAG_TIMING = 1
 FLAG_NO_ZERO = 2
-FLAG_FUSED_ADAM = 4
+FLAG_UNFUSED_ADAM = 8
 K_COMMIT, K_SAMPLE, K_GATHER, K_HEAD_FWD, K_OUT_FWD_DW, K_OUT_DH, K_HEAD_BWD, K_ALLREDUCE, K_ADAM, K_LOSS = range(10)
 KERNEL_NAMES = ["commit", "sample", "gather", "head_fwd", "out_fwd_dw", "out_dh", "head_bwd", "allreduce",
                 "adam", "loss"]
