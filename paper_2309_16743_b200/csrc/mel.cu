@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <ctime>
 #include <string>
 #include <vector>
 
@@ -52,9 +53,10 @@ struct mel_ctx {
   StMeta* h_stmeta = nullptr;      // pinned ring mirror of staging metadata
   uint64_t tail = 0;               // accepted puts
   uint64_t known_consumed = 0;
+  bool copy_fence = false;                  // see ensure_ring_space
   bool closed = false;
   bool copy_pending = false;
-  cudaEvent_t ev_copy = nullptr;
+  cudaEvent_t ev_copy = nullptr, ev_fence = nullptr;
   int32_t* d_slots = nullptr;
   bool batch_known = false;        // host knows the last batch size
   uint32_t batch_n = 0;
@@ -233,13 +235,31 @@ int validate(const mel_config* g, int world, mel_ctx* c) {
   return MEL_OK;
 }
 
+// A put needs a free staging entry.  The commit kernel publishes its progress in the
+// mapped mirror, so instead of draining the stream the host polls it while the queued
+// steps run (the host may be many steps ahead); only an idle stream with the ring still
+// full is back-pressure (MEL_EAGAIN).  Entries freed this way may still be read by a
+// queued commit_copy, so the next host-buffer put fences the copy stream (copy_fence).
 int ensure_ring_space(mel_ctx* c) {
   const uint32_t S = c->cfg.staging_entries;
   if (c->tail - c->known_consumed < S) return MEL_OK;
-  int r = sync_stream(c);
-  if (r) return r;
-  if (c->tail - c->known_consumed < S) return MEL_OK;
-  return MEL_EAGAIN;
+  for (;;) {
+    const uint64_t seen = *reinterpret_cast<volatile uint64_t*>(&c->h_mirror->consumed);
+    if (seen > c->known_consumed) {
+      c->known_consumed = seen;
+      c->copy_fence = true;
+    }
+    if (c->tail - c->known_consumed < S) return MEL_OK;
+    const cudaError_t q = cudaStreamQuery(c->stream);
+    if (q == cudaSuccess) {
+      int r = sync_stream(c);
+      if (r) return r;
+      return c->tail - c->known_consumed < S ? MEL_OK : MEL_EAGAIN;
+    }
+    if (q != cudaErrorNotReady) return fail(c, MEL_ECUDA, "stream query: %s", cudaGetErrorString(q));
+    struct timespec ts{0, 20000};
+    nanosleep(&ts, nullptr);
+  }
 }
 
 int commit(mel_ctx* c) {
@@ -524,6 +544,7 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
   else { CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)); c->own_stream = true; }
   CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_fence, cudaEventDisableTiming));
 
   // geometry: dims = [6, hidden..., N]
   c->dims[0] = 6;
@@ -718,6 +739,7 @@ void mel_destroy(mel_ctx* c) {
   if (c->h_mirror) cudaFreeHost(c->h_mirror);
   if (c->h_stmeta) cudaFreeHost(c->h_stmeta);
   if (c->ev_copy) cudaEventDestroy(c->ev_copy);
+  if (c->ev_fence) cudaEventDestroy(c->ev_fence);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -836,6 +858,11 @@ int reservoir_put(mel_ctx* c, uint32_t sim, uint32_t t, const float X[5], const 
     CK(cudaMemcpyAsync(dmeta, &c->h_stmeta[e], sizeof(StMeta), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(dst, field, 4ull * c->N, cudaMemcpyDeviceToDevice, c->stream));
   } else {
+    if (c->copy_fence) {
+      CK(cudaEventRecord(c->ev_fence, c->stream));
+      CK(cudaStreamWaitEvent(c->copy_stream, c->ev_fence, 0));
+      c->copy_fence = false;
+    }
     CK(cudaMemcpyAsync(dmeta, &c->h_stmeta[e], sizeof(StMeta), cudaMemcpyHostToDevice, c->copy_stream));
     CK(cudaMemcpyAsync(dst, field, 4ull * c->N, cudaMemcpyHostToDevice, c->copy_stream));
     CK(cudaEventRecord(c->ev_copy, c->copy_stream));

@@ -301,7 +301,7 @@ class Context:
     def kernel_time_reset(self):
         self._check(self.lib.mel_kernel_time_reset(self.h))
 
-    def debug_counters(self, n: int = 160 * 32):
+    def debug_counters(self, n: int = 160 * 32 + 64 * 8 + 17 * 8):
         out = np.zeros(n, dtype=np.uint64)
         self._check(self.lib.mel_debug_counters(self.h, out.ctypes.data_as(C.POINTER(C.c_uint64)), n))
         return out
