@@ -334,20 +334,30 @@ def main():
     P = peaks()
     K = HIDDEN[-1]
     n_params = ctx.n_params
-    alg = {
-        "out_fwd_dw": ("tensor", 4.0 * B * n_field * K),                    # Y = H W^T and dW = dY^T H
-        "out_dh": ("tensor", 2.0 * B * n_field * K),                        # dH = dY W
-        "adam": ("hbm", 28.0 * n_params + 2.0 * n_field * K),               # p,m,v,g in; p,m,v out; bf16 W shadow
+    # algorithmic work per launch (SURVEY §8(d) per-unit figures x units):
+    # flops of the GEMMs; bytes the algorithm must move (not this design's dY^T round trip)
+    fused = world == 1 and not (args.flags & mel.FLAG_UNFUSED_ADAM)
+    n_small = n_params - n_field * K                                    # head + biases
+    k1_bytes = n_field * (2.0 * K + 2.0 * B + (26.0 * K if fused else 4.0 * K))
+    alg = {   # name: (flops, bytes)
+        "out_fwd_dw": (4.0 * B * n_field * K, k1_bytes),                # Y = H W^T, dW = dY^T H (+ Adam of W_L if fused)
+        "out_dh": (2.0 * B * n_field * K, 2.0 * n_field * K),           # dH = dY W
+        "adam": (0.0, 28.0 * (n_small if fused else n_params) + (0.0 if fused else 2.0 * n_field * K)),
     }
+    tpeak = P.get("bf16_tflops_sustained", P.get("bf16_tflops"))
+
+    def fracs(name):
+        f_, b_ = alg[name]
+        d = kernels[name]["ms_per_step"] / 1e3
+        if d <= 0:
+            return None
+        return {"tensor": (f_ / d / 1e12, tpeak, "TFLOP/s"), "hbm": (b_ / d / 1e9, P["hbm_gbs"], "GB/s")}
+
     dom = max(alg, key=lambda n: kernels[n]["ms_per_step"])
-    bound, work = alg[dom]
-    dur_s = kernels[dom]["ms_per_step"] / 1e3
-    if bound == "tensor":
-        peak, unit_r = P.get("bf16_tflops_sustained", P.get("bf16_tflops")), "TFLOP/s"
-        achieved = work / dur_s / 1e12
-    else:
-        peak, unit_r = P["hbm_gbs"], "GB/s"
-        achieved = work / dur_s / 1e9
+    fr = fracs(dom)
+    bound = max(fr, key=lambda k: fr[k][0] / fr[k][1])
+    achieved, peak, unit_r = fr[bound]
+    other = "tensor" if bound == "hbm" else "hbm"
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
@@ -357,12 +367,17 @@ def main():
         pass
     roofline = {"kernel": dom, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit_r,
                 "frac": achieved / peak, "traffic": traffic,
-                "peak_source": "MEASURED_PEAKS.json %s" % ("bf16_tflops_sustained" if bound == "tensor" else "hbm_gbs")}
-    for name, (b_, w_) in alg.items():
-        d = kernels[name]["ms_per_step"] / 1e3
-        if d > 0:
-            kernels[name]["achieved"] = w_ / d / (1e12 if b_ == "tensor" else 1e9)
-            kernels[name]["unit"] = "TFLOP/s" if b_ == "tensor" else "GB/s"
+                "peak_source": "MEASURED_PEAKS.json %s" % ("bf16_tflops_sustained" if bound == "tensor" else "hbm_gbs"),
+                "secondary": {"bound": other, "achieved": fr[other][0], "unit": fr[other][2],
+                              "frac": fr[other][0] / fr[other][1]},
+                "algorithmic_bytes": alg[dom][1], "algorithmic_flops": alg[dom][0], "fused_adam": fused}
+    for name in alg:
+        f2 = fracs(name)
+        if f2:
+            b2 = max(f2, key=lambda k: f2[k][0] / f2[k][1])
+            kernels[name]["achieved"] = f2[b2][0]
+            kernels[name]["unit"] = f2[b2][2]
+            kernels[name]["frac"] = f2[b2][0] / f2[b2][1]
     step_flops = (6.0 * B * n_field * K + 6.0 * B * K * K + 4.0 * B * 6 * K)
     tensor_frac_step = step_flops / (ms_step / 1e3) / 1e12 / P["bf16_tflops"]
 
