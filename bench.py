@@ -290,8 +290,8 @@ def main():
             allc = ctx.debug_counters()
             raw = allc[:160 * 32].reshape(160, 32)
             prof = raw[:148].astype(np.float64)
-            tl = allc[160 * 32:160 * 32 + 512].reshape(64, 8).astype(np.int64)
-            tl2 = allc[160 * 32 + 512:].reshape(17, 8).astype(np.int64)
+            tl = allc[160 * 32:160 * 32 + 768].reshape(64, 12).astype(np.int64)
+            tl2 = allc[160 * 32 + 768:].reshape(17, 8).astype(np.int64)
             names = {0: "mma_total", 1: "mma_w_full", 2: "mma_h_full", 3: "mma_y_empty", 4: "mma_dy_full",
                      5: "mma_dw_empty", 6: "mma_fwd_issue", 7: "mma_dw_issue", 8: "epi_total", 9: "epi_t_full", 10: "epi_y_full", 11: "epi_dy_empty",
                      12: "epi_store_bar", 13: "epi_dw_readout", 14: "epi_db_bar", 16: "tma_total", 17: "tma_w_empty",
@@ -300,10 +300,11 @@ def main():
             print(json.dumps({"ms_per_step": ms_step, "value": value, "k1_wait_cycles_mean_per_cta": k1}), flush=True)
             # CTA 0 timeline of the last launch, cycles relative to the MMA warp's tile start
             # (0 W ready, 1 H chunk 0 ready, 2 targets chunk 0, 3 Y chunk 0, 4 dW done,
-            #  5 Adam done, 6 producer resumes, 7 loader resumes)
+            #  5 Adam / send done, 6 producer resumes, 7 loader resumes, 8 peers' dW arrived,
+            #  9 send performed at the owner, 10 send issued)
             nt = int(np.count_nonzero(tl[:, 0]))
             for t in range(min(nt, 60)):
-                print("tile %2d: " % t + " ".join("%8d" % (tl[t, k] - tl[t, 0]) for k in range(8)) +
+                print("tile %2d: " % t + " ".join("%8d" % (tl[t, k] - tl[t, 0] if tl[t, k] else 0) for k in range(11)) +
                       ("  period %d" % (tl[t + 1, 0] - tl[t, 0]) if t + 1 < nt else ""))
             # tile 5 per chunk: 0 fwd issue, 1 dW issue, 2 epilogue has Y, 3 dY in TMEM, 4 epilogue done
             for c in range(16):

@@ -99,6 +99,10 @@ typedef struct {
                                     stored gradient instead of inside the output-layer kernel's
                                     dW epilogue (the default there).  Read at
                                     mel_create only.                                        */
+#define MEL_FLAG_NCCL_EXCHANGE 16u /* world > 1, bf16: NCCL reduce-scatter of dW_L + sharded Adam
+                                      kernel + shadow all-gather instead of the in-kernel NVLink
+                                      exchange (the default when every GPU pair has peer access;
+                                      DESIGN §10).  Read at mel_create only.                     */
 #define MEL_FLAG_NO_ZERO 2u    /* world > 1, bf16: plain all-reduce + replicated Adam instead of
                                   reduce-scatter / sharded Adam / shadow all-gather            */
 

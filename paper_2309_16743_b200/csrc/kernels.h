@@ -51,6 +51,7 @@ struct StepDev {
   uint64_t k, S;       // Adam step, global samples consumed
   int32_t skip;        // no samples this step
   int32_t nonfinite;
+  double n_glob;       // this rank's batch size, all-reduced ahead of K1 (exchange mode)
 };
 
 struct ResArgs {
@@ -105,7 +106,8 @@ void reduce_local(StepDev* sd, const double* parts, int n_parts, const ResDev* s
 void step_finalize(StepDev* sd, double n_field, double lr0, double lr_min, uint64_t halving, double b1, double b2,
                    Mirror* mirror, ResDev* st, cudaStream_t s);
 void step_prepare(StepDev* sd, const ResDev* st, double n_field, double lr0, double lr_min, uint64_t halving, double b1,
-                  double b2, cudaStream_t s);
+                  double b2, cudaStream_t s, bool global_n = false);   // global_n: use sd->n_glob
+void stage_count(StepDev* sd, const ResDev* st, cudaStream_t s);     // sd->n_glob = st->n_last
 void adam_flat(float* p, float* m, float* v, const float* g, uint64_t n, const StepDev* sd,
                float b1, float b2, float eps, __nv_bfloat16* shadow, uint64_t sh_begin, uint64_t sh_end,
                cudaStream_t s);

@@ -100,6 +100,17 @@ struct mel_ctx {
   uint32_t bt0[NBMAX] = {}, bt1[NBMAX] = {};
   cudaEvent_t ev_k1[NBMAX] = {}, ev_agb[NBMAX] = {};
   int sm_reserve = 0;
+  // in-kernel exchange (world > 1, bf16, default; MEL_FLAG_NCCL_EXCHANGE turns it off):
+  // every rank TMA-reduce-adds the dW tiles it does not own into the owner's acc over
+  // NVLink (CUDA IPC mappings), owners run the fused Adam and write the bf16 shadow rows to
+  // every rank from inside K1; only the small region + [SSE, n] go through NCCL
+  bool peer = false;
+  float* d_acc = nullptr;                   // [Npad][Klast] fp32, peers' dW sum (owned tiles' rows)
+  uint32_t* d_cnt = nullptr;                // [Npad / 128] arrival counters (owned tiles)
+  float* p_acc[tc::MAX_WORLD] = {};         // every rank's acc / counters / shadows (IPC)
+  uint32_t* p_cnt[tc::MAX_WORLD] = {};
+  __nv_bfloat16* p_sh[2][tc::MAX_WORLD] = {};
+  uint32_t epoch = 0;
 
   // timing
   std::vector<TimedPair> pending;
@@ -341,6 +352,18 @@ int wait_shadow(mel_ctx* c) {
 int gather_master(mel_ctx* c, bool moments) {
   if (!c->zero) return MEL_OK;
   const uint64_t offW = c->off[2 * (c->L - 1)];
+  if (c->peer) {
+    // owners are interleaved by tile (tc::tile_owner): every rank contributes its owned
+    // rows and zeros elsewhere; an integer sum of the bit patterns is an exact gather.
+    // The W_L gradient region is free scratch in this mode.
+    float* arrs[3] = {c->d_p + offW, c->d_m + offW, c->d_v + offW};
+    float* tmp = c->d_g + offW;
+    for (int i = 0; i < (moments ? 3 : 1); ++i) {
+      tc::owned_rows(c->tcb, arrs[i], tmp, c->Klast, c->rank, c->world, c->stream);
+      NK(ncclAllReduce(tmp, arrs[i], c->Npad * c->Klast, ncclUint32, ncclSum, c->comm, c->stream));
+    }
+    return MEL_OK;
+  }
   CK(cudaEventRecord(c->ev_head, c->stream));
   CK(cudaStreamWaitEvent(c->comm_stream, c->ev_head, 0));
   NK(ncclGroupStart());
@@ -447,16 +470,27 @@ int train_step_bf16(mel_ctx* c) {
   a.N = c->N; a.Npad = c->Npad; a.B = B; a.K = K;
   a.shadow_idx = c->shadow_cur;
   a.w_bf16 = c->d_shadow[c->shadow_cur];
-  a.fused_adam = c->fused_adam ? 1 : 0;
-  if (c->fused_adam) {
+  a.fused_adam = (c->fused_adam || c->peer) ? 1 : 0;
+  if (a.fused_adam) {
     const uint64_t offW = c->off[2 * (L - 1)];
     a.adam_p = c->d_p + offW; a.adam_m = c->d_m + offW; a.adam_v = c->d_v + offW;
     a.shadow_out = c->d_shadow[c->shadow_cur ^ 1];
     a.sd = c->d_sd;
     a.b1 = (float)c->cfg.beta1; a.b2 = (float)c->cfg.beta2; a.eps = (float)c->cfg.eps;
+    if (c->peer) {
+      // the Adam inside K1 needs the global batch size (gradient scale, skip) up front
+      Timer t(c, MEL_K_ALLREDUCE, 1);
+      stage_count(c->d_sd, c->d_st, c->stream);
+      NK(ncclAllReduce(&c->d_sd->n_glob, &c->d_sd->n_glob, 1, ncclFloat64, ncclSum, c->comm, c->stream));
+    }
     Timer t(c, MEL_K_LOSS, 1);
     step_prepare(c->d_sd, c->d_st, (double)c->N, c->cfg.lr0, c->cfg.lr_min, c->cfg.lr_halving_samples,
-                 c->cfg.beta1, c->cfg.beta2, c->stream);
+                 c->cfg.beta1, c->cfg.beta2, c->stream, c->peer);
+  }
+  if (c->peer) {
+    a.peer = 1; a.rank = (uint32_t)c->rank; a.world = (uint32_t)c->world; a.epoch = ++c->epoch;
+    a.cnt_local = c->d_cnt;
+    for (int q = 0; q < c->world; ++q) { a.cnt_peer[q] = c->p_cnt[q]; a.sh_peer[q] = c->p_sh[c->shadow_cur ^ 1][q]; }
   }
   a.b = c->d_p + c->off[2 * (L - 1) + 1];
   a.h_bf16 = c->tcb.h_bf16;
@@ -470,7 +504,7 @@ int train_step_bf16(mel_ctx* c) {
   a.dz = c->d_dz[L - 2];
   a.z = c->d_z[L - 2];
   int nparts = 0;
-  if (!c->zero) {
+  if (!c->zero || c->peer) {
     int r0 = wait_shadow(c);
     if (r0) return r0;
     Timer t(c, MEL_K_OUT_FWD_DW, 1);
@@ -533,6 +567,66 @@ int mel_nccl_unique_id(void* out128) {
 }
 
 const char* mel_last_error(const mel_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+// In-kernel exchange setup: this rank's acc + counters, then every rank's acc, counters and
+// both shadow buffers mapped through CUDA IPC (handles all-gathered over NCCL).  Needs
+// peer access between every pair of GPUs (NVLink / NVSwitch); otherwise the NCCL exchange
+// stays.  Collective: every rank decides the same (the all-reduced minimum).
+static int setup_peer(mel_ctx* c) {
+  int ok = 1;
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  // the peers' device ordinals are not known here; require access to every visible device
+  for (int d = 0; d < ndev; ++d) {
+    if (d == c->dev) continue;
+    int can = 0;
+    CK(cudaDeviceCanAccessPeer(&can, c->dev, d));
+    if (!can) ok = 0;
+  }
+  const uint64_t rows = c->Npad;
+  const uint32_t tiles = (uint32_t)(rows / 128);
+  int* d_ok;
+  CK(cudaMalloc(&d_ok, sizeof(int)));
+  CK(cudaMemcpy(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice));
+  NK(ncclAllReduce(d_ok, d_ok, 1, ncclInt32, ncclMin, c->comm, c->stream));
+  CK(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(d_ok);
+  if (!ok) return MEL_OK;
+  DALLOC(c->d_acc, rows * c->Klast);
+  DALLOC(c->d_cnt, tiles);
+  CK(cudaMemset(c->d_acc, 0, 4 * rows * c->Klast));
+  CK(cudaMemset(c->d_cnt, 0, 4 * tiles));
+  // handles: [acc, cnt, shadow0, shadow1] per rank
+  const int NH = 4;
+  std::vector<cudaIpcMemHandle_t> mine(NH), all((size_t)NH * c->world);
+  void* bufs[NH] = {c->d_acc, c->d_cnt, c->d_shadow[0], c->d_shadow[1]};
+  for (int i = 0; i < NH; ++i) CK(cudaIpcGetMemHandle(&mine[i], bufs[i]));
+  char* d_h;
+  const size_t hb = sizeof(cudaIpcMemHandle_t) * NH;
+  CK(cudaMalloc(&d_h, hb * c->world));
+  CK(cudaMemcpy(d_h + hb * c->rank, mine.data(), hb, cudaMemcpyHostToDevice));
+  NK(ncclAllGather(d_h + hb * c->rank, d_h, hb, ncclChar, c->comm, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(all.data(), d_h, hb * c->world, cudaMemcpyDeviceToHost));
+  cudaFree(d_h);
+  for (int q = 0; q < c->world; ++q) {
+    if (q == c->rank) {
+      c->p_acc[q] = c->d_acc; c->p_cnt[q] = c->d_cnt;
+      c->p_sh[0][q] = c->d_shadow[0]; c->p_sh[1][q] = c->d_shadow[1];
+      continue;
+    }
+    void* p[NH];
+    for (int i = 0; i < NH; ++i)
+      CK(cudaIpcOpenMemHandle(&p[i], all[(size_t)q * NH + i], cudaIpcMemLazyEnablePeerAccess));
+    c->p_acc[q] = static_cast<float*>(p[0]); c->p_cnt[q] = static_cast<uint32_t*>(p[1]);
+    c->p_sh[0][q] = static_cast<__nv_bfloat16*>(p[2]); c->p_sh[1][q] = static_cast<__nv_bfloat16*>(p[3]);
+  }
+  if (tc::prepare_peer(c->tcb, c->Klast, rows, c->rank, c->world, c->p_acc))
+    return fail(c, MEL_ECUDA, "exchange tensor maps: %s", tc::last_error());
+  c->peer = true;
+  return MEL_OK;
+}
 
 static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, void* stream) {
   int r = validate(g, c->world, c);
@@ -690,6 +784,10 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
       CK(cudaEventCreateWithFlags(&c->ev_k1[j], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_agb[j], cudaEventDisableTiming));
     }
+    if (c->zero && !(g->flags & MEL_FLAG_NCCL_EXCHANGE) && c->world <= tc::MAX_WORLD) {
+      r = setup_peer(c);
+      if (r) return r;
+    }
   }
   return MEL_OK;
 }
@@ -717,6 +815,14 @@ void mel_destroy(mel_ctx* c) {
   cudaSetDevice(c->dev);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+  if (c->peer) {
+    for (int q = 0; q < c->world; ++q) {
+      if (q == c->rank) continue;
+      void* h[] = {c->p_acc[q], c->p_cnt[q], c->p_sh[0][q], c->p_sh[1][q]};
+      for (void* p : h)
+        if (p) cudaIpcCloseMemHandle(p);
+    }
+  }
   if (c->comm) ncclCommDestroy(c->comm);
   cudaEvent_t evs[] = {c->ev_gw, c->ev_head, c->ev_ar, c->ev_adam, c->ev_ag};
   for (cudaEvent_t e : evs)
@@ -732,7 +838,8 @@ void mel_destroy(mel_ctx* c) {
                   c->ra.bitmap, c->ra.pos, c->ra.payload, c->ra.plan, c->d_slots, c->d_p, c->d_m, c->d_v, c->d_g,
                   c->d_shadow[0], c->d_shadow[1], c->d_xn, c->d_z[0], c->d_z[1], c->d_h[0], c->d_h[1], c->d_dz[0],
                   c->d_dz[1], c->d_dy, c->d_part, c->d_sse_part, c->d_sd, c->d_eval_x, c->d_eval_t, c->d_eval_y,
-                  c->d_eval_f, c->d_eval_z[0], c->d_eval_z[1], c->d_eval_h[0], c->d_eval_h[1], c->d_eval_xn};
+                  c->d_eval_f, c->d_eval_z[0], c->d_eval_z[1], c->d_eval_h[0], c->d_eval_h[1], c->d_eval_xn,
+                  c->d_acc, c->d_cnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   tc::free_buffers(c->tcb);
@@ -939,8 +1046,9 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
     step_finalize(c->d_sd, (double)c->N, c->cfg.lr0, c->cfg.lr_min, c->cfg.lr_halving_samples, c->cfg.beta1,
                   c->cfg.beta2, c->d_mirror, c->d_st, c->stream);
   }
-  if (c->fused_adam) {
-    // W_L was updated inside K1 (new shadow in the other buffer); the small region here
+  if (c->fused_adam || c->peer) {
+    // W_L was updated inside K1 (new shadow in the other buffer, written to every rank in
+    // exchange mode); the small region here
     Timer t(c, MEL_K_ADAM, 1);
     adam_flat(c->d_p, c->d_m, c->d_v, c->d_g, c->off[2 * (c->L - 1)], c->d_sd, (float)c->cfg.beta1,
               (float)c->cfg.beta2, (float)c->cfg.eps, nullptr, 0, 0, c->stream);
@@ -971,7 +1079,7 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
     adam_flat(c->d_p, c->d_m, c->d_v, c->d_g, c->n_flat, c->d_sd, (float)c->cfg.beta1, (float)c->cfg.beta2,
               (float)c->cfg.eps, sh, b0, b1, c->stream);
   }
-  if (c->zero) {
+  if (c->zero && !c->peer) {
     Timer t(c, MEL_K_ALLREDUCE, 0, c->comm_stream);
     CK(cudaEventRecord(c->ev_adam, c->stream));
     CK(cudaStreamWaitEvent(c->comm_stream, c->ev_adam, 0));

@@ -238,8 +238,8 @@ __global__ void step_finalize_kernel(StepDev* sd, double n_field, double lr0, do
 // Step scalars ahead of the output-layer kernel (world == 1, fused Adam): the same
 // values step_finalize computes afterwards (scale, lr, bias corrections of step k+1).
 __global__ void step_prepare_kernel(StepDev* sd, const ResDev* st, double n_field, double lr0, double lr_min,
-                                    uint64_t halving, double b1, double b2) {
-  const double n = (double)st->n_last;
+                                    uint64_t halving, double b1, double b2, int global_n) {
+  const double n = global_n ? sd->n_glob : (double)st->n_last;
   if (n <= 0.0) { sd->skip = 1; return; }
   sd->skip = 0;
   sd->scale = (float)(1.0 / (n_field * n));
@@ -437,9 +437,13 @@ void step_finalize(StepDev* sd, double n_field, double lr0, double lr_min, uint6
 }
 
 void step_prepare(StepDev* sd, const ResDev* st, double n_field, double lr0, double lr_min, uint64_t halving, double b1,
-                  double b2, cudaStream_t s) {
-  step_prepare_kernel<<<1, 1, 0, s>>>(sd, st, n_field, lr0, lr_min, halving, b1, b2);
+                  double b2, cudaStream_t s, bool global_n) {
+  step_prepare_kernel<<<1, 1, 0, s>>>(sd, st, n_field, lr0, lr_min, halving, b1, b2, global_n ? 1 : 0);
 }
+
+__global__ void stage_count_kernel(StepDev* sd, const ResDev* st) { sd->n_glob = (double)st->n_last; }
+
+void stage_count(StepDev* sd, const ResDev* st, cudaStream_t s) { stage_count_kernel<<<1, 1, 0, s>>>(sd, st); }
 
 void adam_flat(float* p, float* m, float* v, const float* g, uint64_t n, const StepDev* sd, float b1, float b2,
                float eps, __nv_bfloat16* shadow, uint64_t sh_begin, uint64_t sh_end, cudaStream_t s) {

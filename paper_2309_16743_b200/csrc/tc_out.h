@@ -21,6 +21,14 @@ struct TcBuffers {
   int fwd_ctas = 0;
 };
 
+constexpr int MAX_WORLD = 8;
+
+// In-kernel exchange: owner rank of W_L tile t (128 rows) when K1 runs on G CTAs, tile
+// t = b + G*i going to CTA b in its i-th iteration.  Every CTA alternates between tiles it
+// owns and tiles it sends, and every wave splits evenly across owners, so both NVLink
+// directions stay busy and no CTA carries more Adam work than another.
+__host__ __device__ inline uint32_t tile_owner(uint32_t t, uint32_t G, uint32_t R) { return (t % G + t / G) % R; }
+
 struct OutTcArgs {
   uint32_t N, B, K;
   uint64_t Npad;
@@ -43,9 +51,24 @@ struct OutTcArgs {
   __nv_bfloat16* shadow_out;         // updated bf16 shadow (fused), the other buffer
   const StepDev* sd;                 // step scalars (scale, lr, bias corrections, skip)
   float b1, b2, eps;
+  // in-kernel exchange (world > 1, bf16; tc_out.cu K1Params): the fused Adam runs on the
+  // tiles this rank owns, the other tiles' dW are reduce-added into their owners' acc
+  int peer;
+  uint32_t rank, world, epoch;
+  uint32_t* cnt_local;
+  uint32_t* cnt_peer[MAX_WORLD];
+  __nv_bfloat16* sh_peer[MAX_WORLD];
 };
 
 int alloc_buffers(TcBuffers& t, uint64_t Npad, uint32_t B, uint32_t K);
+// tensor maps of the in-kernel exchange: this rank's acc and every rank's (peer-mapped) acc
+int prepare_peer(TcBuffers& t, uint32_t K, uint64_t rows, int rank, int world, float* const* acc);
+// dst = src on the rows of the tiles `rank` owns, 0 elsewhere ([Npad][K] fp32)
+void owned_rows(const TcBuffers& t, const float* src, float* dst, uint32_t K, int rank, int world, cudaStream_t s);
+inline uint32_t k1_grid(const TcBuffers& t) {                // CTAs of a full-range K1 launch
+  const uint32_t tiles = (uint32_t)(t.Npad / 128);
+  return tiles < (uint32_t)t.fwd_ctas ? tiles : (uint32_t)t.fwd_ctas;
+}
 void free_buffers(TcBuffers& t);
 int prepare(TcBuffers& t, uint64_t Npad, uint32_t B, uint32_t K, const __nv_bfloat16* const* w_bf16,
             const __nv_bfloat16* payload, uint32_t capacity, const float* grad_w, int sm_reserve,

@@ -20,6 +20,7 @@ STORE_F32, STORE_BF16 = 0, 1
 FLAG_TIMING = 1
 FLAG_NO_ZERO = 2
 FLAG_UNFUSED_ADAM = 8
+FLAG_NCCL_EXCHANGE = 16
 K_COMMIT, K_SAMPLE, K_GATHER, K_HEAD_FWD, K_OUT_FWD_DW, K_OUT_DH, K_HEAD_BWD, K_ALLREDUCE, K_ADAM, K_LOSS = range(10)
 KERNEL_NAMES = ["commit", "sample", "gather", "head_fwd", "out_fwd_dw", "out_dh", "head_bwd", "allreduce",
                 "adam", "loss"]
@@ -301,7 +302,7 @@ class Context:
     def kernel_time_reset(self):
         self._check(self.lib.mel_kernel_time_reset(self.h))
 
-    def debug_counters(self, n: int = 160 * 32 + 64 * 8 + 17 * 8):
+    def debug_counters(self, n: int = 160 * 32 + 64 * 12 + 17 * 8):
         out = np.zeros(n, dtype=np.uint64)
         self._check(self.lib.mel_debug_counters(self.h, out.ctypes.data_as(C.POINTER(C.c_uint64)), n))
         return out

@@ -31,6 +31,8 @@ def main():
     from paper_2309_16743_b200 import mel
 
     mode = sys.argv[1] if len(sys.argv) > 1 else "fp32"
+    # bf16: in-kernel NVLink exchange (default); bf16-nccl: NCCL reduce-scatter / all-gather
+    flags = mel.FLAG_NCCL_EXCHANGE if mode.endswith("-nccl") else 0
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(rank)
     dist.init_process_group("gloo")
@@ -40,13 +42,13 @@ def main():
         wl = replace(design.TINY_EVICT, world=world, puts_per_step=10)
         prec = store = 0
         tol_loss, tol_w, max_steps = 1e-5, 1e-5, None
-    else:
+    else:   # bf16, bf16-nccl
         wl = replace(design.MEDIUM, name="medium-bf16-mr", capacity=600, threshold=100, sims=30, world=world,
                      batch=128, puts_per_step=60)
         prec = store = 1
         tol_loss, tol_w, max_steps = 2e-2, 1e-3, 5
     table = FieldTable(wl)
-    ctx = mel.Context(make_config(wl, precision=prec, storage=store), rank=rank, world=world, nccl_id=obj[0],
+    ctx = mel.Context(make_config(wl, precision=prec, storage=store, flags=flags), rank=rank, world=world, nccl_id=obj[0],
                       device=rank)
     res = [ores.Reservoir(wl.capacity, wl.threshold, wl.n_field, seed=1, rank=r, storage=store) for r in range(world)]
     batches = [[] for _ in range(world)]

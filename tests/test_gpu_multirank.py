@@ -15,14 +15,17 @@ def _ngpu():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("mode", ["fp32", "bf16"])
-def test_two_rank_parity_nccl(mode):
-    if _ngpu() < 2:
-        pytest.skip("needs 2 GPUs")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+@pytest.mark.parametrize("world,mode", [(2, "fp32"), (2, "bf16"), (2, "bf16-nccl"), (4, "bf16")])
+def test_multi_rank_parity(world, mode):
+    """fp32: NCCL all-reduce; bf16: the in-kernel NVLink exchange (dW tiles reduce-added
+    into their owner's buffer, fused Adam at the owner, shadow rows pushed to every rank);
+    bf16-nccl: reduce-scatter / sharded Adam / all-gather through NCCL."""
+    if _ngpu() < world:
+        pytest.skip("needs %d GPUs" % world)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=%d" % world,
            "--master-addr=127.0.0.1", "--master-port=%d" % (29600 + os.getpid() % 300),
            os.path.join(HERE, "mp_gpu_parity.py"), mode]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
-    assert r.stdout.count("replicas identical") == 2
+    assert r.stdout.count("replicas identical") == world
