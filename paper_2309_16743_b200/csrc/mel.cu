@@ -622,7 +622,7 @@ static int setup_peer(mel_ctx* c) {
     c->p_acc[q] = static_cast<float*>(p[0]); c->p_cnt[q] = static_cast<uint32_t*>(p[1]);
     c->p_sh[0][q] = static_cast<__nv_bfloat16*>(p[2]); c->p_sh[1][q] = static_cast<__nv_bfloat16*>(p[3]);
   }
-  if (tc::prepare_peer(c->tcb, c->Klast, rows, c->rank, c->world, c->p_acc))
+  if (tc::prepare_peer(c->tcb, c->Klast, rows, c->rank, c->world, c->p_acc, c->p_sh[0], c->p_sh[1]))
     return fail(c, MEL_ECUDA, "exchange tensor maps: %s", tc::last_error());
   c->peer = true;
   return MEL_OK;

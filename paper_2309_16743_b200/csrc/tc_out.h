@@ -62,7 +62,8 @@ struct OutTcArgs {
 
 int alloc_buffers(TcBuffers& t, uint64_t Npad, uint32_t B, uint32_t K);
 // tensor maps of the in-kernel exchange: this rank's acc and every rank's (peer-mapped) acc
-int prepare_peer(TcBuffers& t, uint32_t K, uint64_t rows, int rank, int world, float* const* acc);
+int prepare_peer(TcBuffers& t, uint32_t K, uint64_t rows, int rank, int world, float* const* acc,
+                 __nv_bfloat16* const* sh0, __nv_bfloat16* const* sh1);
 // dst = src on the rows of the tiles `rank` owns, 0 elsewhere ([Npad][K] fp32)
 void owned_rows(const TcBuffers& t, const float* src, float* dst, uint32_t K, int rank, int world, cudaStream_t s);
 inline uint32_t k1_grid(const TcBuffers& t) {                // CTAs of a full-range K1 launch
