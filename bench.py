@@ -63,7 +63,11 @@ def config_block(args, world):
             "batch_per_rank": args.batch, "global_batch": args.batch * world, "puts_per_step": args.puts_per_step,
             "routing": "(sim + t) mod R", "precision": "bf16 tcgen05 output layer, fp32 master/Adam",
             "target_storage": "bf16", "l2": "inputs larger than L2 (W 0.5 GB, Adam state 3 GB, targets 2 GB / step)",
-            "parallelism": "dp%d" % world}
+            "parallelism": "dp%d" % world,
+            "exchange": ("none" if world == 1 else
+                         "NCCL reduce-scatter + sharded Adam + shadow all-gather" if args.flags & 16 else
+                         "in-kernel over NVLink: dW tiles TMA-stored/reduce-added into the owner rank, fused Adam at "
+                         "the owner, bf16 shadow rows pushed to every rank; NCCL for the 1.3 MB head + biases")}
 
 
 # ------------------------------------------------------------------------------------
@@ -337,9 +341,11 @@ def main():
     n_params = ctx.n_params
     # algorithmic work per launch (SURVEY §8(d) per-unit figures x units):
     # flops of the GEMMs; bytes the algorithm must move (not this design's dY^T round trip)
-    fused = world == 1 and not (args.flags & mel.FLAG_UNFUSED_ADAM)
+    # fused: the Adam of W_L runs inside K1 (world 1, or the in-kernel NVLink exchange at
+    # world > 1, where each rank updates the 1/R of the rows it owns)
+    fused = (not (args.flags & mel.FLAG_UNFUSED_ADAM)) if world == 1 else not (args.flags & mel.FLAG_NCCL_EXCHANGE)
     n_small = n_params - n_field * K                                    # head + biases
-    k1_bytes = n_field * (2.0 * K + 2.0 * B + (26.0 * K if fused else 4.0 * K))
+    k1_bytes = n_field * (2.0 * K + 2.0 * B + (26.0 * K / world if fused else 4.0 * K))
     alg = {   # name: (flops, bytes)
         "out_fwd_dw": (4.0 * B * n_field * K, k1_bytes),                # Y = H W^T, dW = dY^T H (+ Adam of W_L if fused)
         "out_dh": (2.0 * B * n_field * K, 2.0 * n_field * K),           # dH = dY W
@@ -372,6 +378,15 @@ def main():
                 "secondary": {"bound": other, "achieved": fr[other][0], "unit": fr[other][2],
                               "frac": fr[other][0] / fr[other][1]},
                 "algorithmic_bytes": alg[dom][1], "algorithmic_flops": alg[dom][0], "fused_adam": fused}
+    if world > 1 and fused and dom == "out_fwd_dw":
+        # bytes each rank must push over NVLink per launch: its dW of the rows other ranks own
+        # (fp32) and the new bf16 shadow of its own rows to every other rank
+        nv_bytes = (world - 1) / world * n_field * K * 4.0 + (world - 1) / world * n_field * K * 2.0
+        nv_peak = P.get("nvlink_gbs", 770.0)
+        nv_ach = nv_bytes / (kernels[dom]["ms_per_step"] / 1e3) / 1e9
+        roofline["nvlink"] = {"bytes_per_launch": nv_bytes, "achieved": nv_ach, "peak": nv_peak, "unit": "GB/s",
+                              "frac": nv_ach / nv_peak,
+                              "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s per direction"}
     for name in alg:
         f2 = fracs(name)
         if f2:
