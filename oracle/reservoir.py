@@ -26,6 +26,19 @@ readings R1-R7 (readings Q1-Q9):
                     pos[k] = pos[p-1]; p -= 1
   CLOSE():    if closed -> EPROTO.  closed = true; COMMIT()
 
+The two comparison buffers of P:221-223 share the put / pending / commit-point
+machinery (reading R21):
+  FIFO: COMMIT appends while p < C at slot (h + p) mod C (a ring; a full buffer
+        suspends production = puts stay pending).  SAMPLE(B) takes the B oldest
+        items (slots h..h+B-1 mod C) and removes them; during reception it needs
+        p >= B ("as soon as the buffer can provide one"), after close it returns
+        min(B, p).  Each item is seen exactly once.
+  FIRO: COMMIT appends while p < C at list position p (slot pos[p]).  SAMPLE(B)
+        makes B draws, each k = bounded_DRAIN(d)(p) over the current list with
+        removal (swap with the last position); during reception every one of the
+        B draws must see more than theta items, i.e. p >= theta + B; the
+        threshold is 0 after close ("set to zero once data production is over").
+
 Stored payload (reading R8, P:210 fp32 wire data, normalisation reading Q13):
   F32 storage : RN_f32((u_f32 - 100f) / 400f)
   BF16 storage: RNE_bf16(RN_f32((u_f32 - 100f) / 400f))
@@ -42,6 +55,7 @@ import numpy as np
 from . import philox
 
 OK, EAGAIN, ECLOSED, EPROTO = 0, 1, -2, -3
+RESERVOIR, FIFO, FIRO = 0, 1, 2
 HIST_BINS = 64
 
 STORE_F32, STORE_BF16 = 0, 1
@@ -81,10 +95,13 @@ class Reservoir:
     """One rank's Reservoir.  Items are (sim, t, X[5] fp32, field fp32[N])."""
 
     def __init__(self, capacity: int, threshold: int, n_field: int, seed: int = 1,
-                 rank: int = 0, storage: int = STORE_F32, chooser=None, keep_payload=True):
+                 rank: int = 0, storage: int = STORE_F32, chooser=None, keep_payload=True,
+                 policy: int = RESERVOIR):
         if not (0 <= threshold < capacity):
             raise ValueError("require 0 <= threshold < capacity (P:321 uses 1000 < 6000)")
         self.C, self.theta, self.N = capacity, threshold, n_field
+        self.policy = policy
+        self.h = 0                      # FIFO ring head
         self.seed, self.rank, self.storage = seed, rank, storage
         self.keep_payload = keep_payload
         self.choose = chooser if chooser is not None else self._philox_choose
@@ -126,6 +143,9 @@ class Reservoir:
         return int(idx[r])
 
     def commit(self) -> None:
+        if self.policy != RESERVOIR:
+            self._commit_queue()
+            return
         C = self.C
         while self.pend:
             if self.u == C:
@@ -154,9 +174,64 @@ class Reservoir:
         if self.closed and not self.pend:
             self.over = True
 
+    # -- FIFO / FIRO --------------------------------------------------------
+    def _commit_queue(self) -> None:
+        C = self.C
+        while self.pend and self.p < C:                   # full buffer: production suspended
+            sim, t, X, field = self.pend.popleft()
+            j = (self.h + self.p) % C if self.policy == FIFO else int(self.pos[self.p])
+            self.p += 1
+            self.sim[j], self.t[j] = sim, t
+            self.X[j] = X
+            if self.keep_payload and field is not None:
+                self.payload[j] = stored_payload(field, self.storage)
+            self.seen[j] = 0
+            self.put_seq[j] = self.q
+            self.commit_log.append((self.q, j, -1, -1, 0))
+            self.q += 1
+            self.u += 1
+        if self.closed and not self.pend:
+            self.over = True
+
+    def _retire(self, j: int) -> None:
+        self.seen[j] += 1                                 # seen once, then removed
+        self.hist[min(int(self.seen[j]), HIST_BINS - 1)] += 1
+        self.u -= 1
+
+    def _sample_queue(self, B: int):
+        need = (B if self.policy == FIFO else self.theta + B) if not self.over else 1
+        if self.p < need:
+            return EAGAIN, []
+        n = min(B, self.p)
+        out = []
+        if self.policy == FIFO:
+            for b in range(n):
+                j = (self.h + b) % self.C
+                self._retire(j)
+                out.append(j)
+            self.h = (self.h + n) % self.C
+            self.p -= n
+            self.d += n
+            return OK, out
+        for _ in range(n):
+            k = self.choose(philox.TAG_DRAIN, self.d, self.p)
+            self.d += 1
+            j = int(self.pos[k])
+            self._retire(j)
+            out.append(j)
+            self.pos[k], self.pos[self.p - 1] = self.pos[self.p - 1], j   # freed slot -> position p-1
+            self.p -= 1
+        return OK, out
+
     # -- Alg. 1 get (batch-atomic) -----------------------------------------------------
     def sample(self, B: int):
-        """Returns (status, slots).  status EAGAIN during reception while p <= theta."""
+        """Returns (status, slots).  status EAGAIN during reception while p <= theta
+        (Reservoir), p < B (FIFO), p < theta + B (FIRO)."""
+        if self.policy != RESERVOIR:
+            self.commit()
+            if self.over and self.p == 0:
+                return OK, []
+            return self._sample_queue(B)
         self.commit()
         if not self.over:
             if self.p <= self.theta:
@@ -198,6 +273,10 @@ class Reservoir:
 
     # -- observability --------------------------------------------------------------------
     def live_slots(self) -> np.ndarray:
+        if self.policy == FIFO:
+            return np.sort((self.h + np.arange(self.p)) % self.C)
+        if self.policy == FIRO:
+            return np.sort(self.pos[: self.p])
         return np.sort(self.pos[: self.p]) if self.over else np.arange(self.p)
 
     def stats(self) -> dict:
@@ -214,8 +293,11 @@ class Reservoir:
         u = int(np.sum(self.seen[live] == 0))
         assert u == self.u, (u, self.u)
         assert self.u <= C
-        if not self.over:
+        if self.policy == RESERVOIR and not self.over:
             assert np.array_equal(self.pos, np.arange(C)), "pos must be identity in reception"
+        if self.policy != RESERVOIR:
+            assert self.u == self.p, "FIFO / FIRO items are removed when seen"
+            assert sorted(self.pos.tolist()) == list(range(C)), "pos is a permutation"
         # conservation: draws = sum k*hist + sum live seen, once nothing saturates
         if self.hist[-1] == 0:
             assert self.d == int(np.sum(np.arange(HIST_BINS) * self.hist)) + int(np.sum(self.seen[live]))
