@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define MEL_ABI_VERSION 1u
+#define MEL_ABI_VERSION 2u
 #define MEL_HIST_BINS 64
 #define MEL_MAX_TENSORS 6
 
@@ -73,6 +73,15 @@ enum mel_storage {
   MEL_STORE_BF16 = 1  /* slot stores RNE_bf16 of the same fp32 value                    */
 };
 
+enum mel_policy {               /* the training buffer                  */
+  MEL_RESERVOIR = 0, /* Algorithm 1: draws with replacement once p > theta, a put into a
+                        full buffer evicts a random *seen* item (the paper's method)     */
+  MEL_FIFO = 1,      /* queue: a batch is the B oldest items, removed when read; needs
+                        p >= B during reception (B <= C); a full buffer suspends puts   */
+  MEL_FIRO = 2       /* list: B random draws with removal once p >= theta + B (theta + B
+                        <= C); threshold 0 after reservoir_close                         */
+};
+
 typedef struct mel_ctx mel_ctx;
 
 typedef struct {
@@ -92,6 +101,8 @@ typedef struct {
   uint64_t seed;               /* Philox key for SAMPLE/EVICT/DRAIN/INIT streams */
   uint32_t staging_entries;    /* depth of the pending-put ring (>= 1)                   */
   uint32_t flags;              /* MEL_FLAG_*                                             */
+  uint32_t policy;             /* enum mel_policy (ABI v2)                               */
+  uint32_t pad;
 } mel_config;
 
 #define MEL_FLAG_TIMING 1u     /* record CUDA events around every kernel (bench roofline) */

@@ -19,7 +19,7 @@ struct ResDev {
   uint32_t over;       // closed && pending empty
   uint32_t n_last;     // size of the last batch (0 = EAGAIN / empty)
   uint32_t n_plan;     // entries committed by the last commit
-  uint32_t pad;
+  uint32_t head;       // FIFO: ring position of the oldest item
   uint64_t hist[HIST_BINS];
 };
 
@@ -74,6 +74,7 @@ struct ResArgs {
   uint64_t seed;
   uint32_t rank;
   uint2* plan;               // [S] (entry, slot)
+  uint32_t policy;           // 0 Reservoir, 1 FIFO, 2 FIRO (mel_policy)
 };
 
 // reservoir.cu

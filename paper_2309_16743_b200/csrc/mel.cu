@@ -54,6 +54,7 @@ struct mel_ctx {
   uint64_t tail = 0;               // accepted puts
   uint64_t known_consumed = 0;
   bool copy_fence = false;                  // see ensure_ring_space
+  uint64_t drawn = 0;                       // items handed out (FIFO / FIRO remove them)
   bool closed = false;
   bool copy_pending = false;
   cudaEvent_t ev_copy = nullptr, ev_fence = nullptr;
@@ -235,6 +236,10 @@ int validate(const mel_config* g, int world, mel_ctx* c) {
   if (!(g->temp_hi > g->temp_lo)) return fail(c, MEL_EINVAL, "temp_hi must exceed temp_lo");
   if (g->precision > MEL_BF16 || g->storage > MEL_STORE_BF16) return fail(c, MEL_EINVAL, "bad precision/storage");
   if (g->staging_entries == 0) return fail(c, MEL_EINVAL, "staging_entries must be >= 1");
+  if (g->policy > MEL_FIRO) return fail(c, MEL_EINVAL, "unknown buffer policy %u", g->policy);
+  if (g->policy == MEL_FIFO && g->batch > g->capacity) return fail(c, MEL_EINVAL, "FIFO needs batch <= capacity");
+  if (g->policy == MEL_FIRO && (uint64_t)g->threshold + g->batch > g->capacity)
+    return fail(c, MEL_EINVAL, "FIRO needs threshold + batch <= capacity");
   if (g->lr_halving_samples == 0) return fail(c, MEL_EINVAL, "lr_halving_samples must be > 0");
   const uint32_t klast = g->hidden[1] ? g->hidden[1] : g->hidden[0];
   if (g->precision == MEL_BF16) {
@@ -701,6 +706,7 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
   a.st = c->d_st; a.mirror = c->d_mirror; a.st_meta = d_stmeta; a.st_field = d_stfield; a.S = S;
   a.C = C; a.theta = g->threshold; a.Npad = c->Npad; a.N = c->N; a.storage = (int)g->storage;
   a.lo = g->temp_lo; a.span = g->temp_hi - g->temp_lo; a.seed = g->seed; a.rank = (uint32_t)c->rank;
+  a.policy = g->policy;
   launch_init_res(a, c->stream);
   DALLOC(c->d_slots, c->B);
 
@@ -1001,8 +1007,17 @@ int reservoir_sample_batch(mel_ctx* c, int32_t* slots_host, uint32_t* n_host) {
   bool need_sync = slots_host || n_host || c->closed;
   uint32_t n = c->B;
   if (!c->closed) {
-    const uint64_t p = c->tail < c->C ? c->tail : c->C;
-    if (p <= c->cfg.threshold) n = 0;
+    if (c->cfg.policy == MEL_RESERVOIR) {
+      const uint64_t p = c->tail < c->C ? c->tail : c->C;
+      if (p <= c->cfg.threshold) n = 0;
+    } else {
+      // FIFO / FIRO remove what they hand out: every accepted put is drawn, in the
+      // buffer, or pending, and a commit fills the buffer up to C
+      const uint64_t left = c->tail - c->drawn;
+      const uint64_t p = left < c->C ? left : c->C;
+      const uint64_t need = c->cfg.policy == MEL_FIFO ? c->B : (uint64_t)c->cfg.threshold + c->B;
+      if (p < need) n = 0;
+    }
   }
   if (need_sync) {
     r = sync_stream(c);
@@ -1011,6 +1026,7 @@ int reservoir_sample_batch(mel_ctx* c, int32_t* slots_host, uint32_t* n_host) {
   }
   c->batch_known = true;
   c->batch_n = n;
+  c->drawn += n;
   if (n_host) *n_host = n;
   if (slots_host && n) CK(cudaMemcpy(slots_host, c->d_slots, 4ull * n, cudaMemcpyDeviceToHost));
   if (!c->closed && n == 0) return MEL_EAGAIN;

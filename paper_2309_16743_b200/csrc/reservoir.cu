@@ -12,6 +12,10 @@
 //                  seen counters by atomicAdd (order-free), u -= #(0->1); after
 //                  the reception is over, sequential DRAIN draws with removal.
 //   gather_inputs: normalised network inputs (X, t) of the batch (reading Q13).
+// The comparison buffers of P:221-223 (reading R21) reuse the same put / staging /
+// commit machinery: commit appends while p < C (FIFO at ring slot head + p, FIRO at
+// list position p -> slot pos[p]); FIFO sampling takes the B oldest items, FIRO makes
+// B DRAIN-stream draws with removal (swap with the last list position, in SMEM).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -48,8 +52,40 @@ __device__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp) {
   return r;
 }
 
+// FIFO / FIRO commit: append the pending puts while the buffer has room
+__device__ void commit_queue(const ResArgs& a, uint64_t tail, uint32_t closed) {
+  ResDev* st = a.st;
+  const uint32_t p = st->p, u = st->u, head = st->head;
+  const uint64_t q = st->q, consumed = st->consumed;
+  uint32_t cnt = 0;
+  if (consumed < tail && p < a.C) {
+    const uint64_t avail = tail - consumed, room = a.C - p;
+    cnt = (uint32_t)(avail < room ? avail : room);
+  }
+  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const uint32_t j = a.policy == 1 ? (head + p + i) % a.C : a.pos[p + i];
+    const uint32_t e = (uint32_t)((consumed + i) % a.S);
+    a.meta[j] = a.st_meta[e];
+    a.seen[j] = 0;
+    a.put_seq[j] = q + i;
+    a.plan[i] = make_uint2(e, j);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st->p = p + cnt; st->u = u + cnt; st->q = q + cnt; st->consumed = consumed + cnt; st->n_plan = cnt;
+    if (closed && consumed + cnt == tail) st->over = 1;
+    Mirror* m = a.mirror;
+    m->consumed = consumed + cnt; m->q = q + cnt; m->p = p + cnt; m->u = u + cnt; m->over = st->over;
+    m->evictions = st->evictions; m->d = st->d;
+  }
+}
+
 __global__ void __launch_bounds__(CTRL_THREADS, 1)
 commit_ctrl(ResArgs a, uint64_t tail, uint32_t closed) {
+  if (a.policy != 0) {
+    commit_queue(a, tail, closed);
+    return;
+  }
   extern __shared__ uint32_t s_bits[];          // seen bitmap, ceil(C/32) words
   __shared__ uint32_t s_warp[32];
   __shared__ uint32_t s_cmd[4];                  // 0: mode (0 stop, 1 fill, 2 evict), 1: count / r, 2: result slot
@@ -173,6 +209,72 @@ commit_copy(ResArgs a) {
 
 constexpr int SAMPLE_THREADS = 1024;
 
+// retire a FIFO / FIRO item: seen once, then removed (hist[1] counts it)
+__device__ __forceinline__ void finish_queue_batch(const ResArgs& a, uint32_t p, uint32_t n, uint64_t d_new) {
+  ResDev* st = a.st;
+  st->hist[1] += n;
+  st->u -= n;
+  st->p = p - n;
+  st->d = d_new;
+  st->n_last = n;
+  Mirror* m = a.mirror;
+  m->p = p - n; m->u = st->u; m->d = d_new; m->n_last = n; m->over = st->over;
+}
+
+// FIFO: the n oldest items, n = B during reception (needs p >= B), min(B, p) after
+__global__ void __launch_bounds__(SAMPLE_THREADS, 1)
+fifo_sample_kernel(ResArgs a, int32_t* slots, uint32_t B) {
+  ResDev* st = a.st;
+  const uint32_t p = st->p, head = st->head;
+  const uint32_t n = st->over ? (p < B ? p : B) : (p >= B ? B : 0u);
+  for (uint32_t b = threadIdx.x; b < n; b += blockDim.x) {
+    const uint32_t j = (head + b) % a.C;
+    slots[b] = (int32_t)j;
+    a.seen[j] = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st->head = (head + n) % a.C;
+    finish_queue_batch(a, p, n, st->d + n);
+  }
+}
+
+// FIRO: n draws k_b = bounded_DRAIN(d + b)(p - b) over the shrinking list, each
+// removing its item by swapping it with the last list position.  The draws are computed
+// in parallel (they depend only on p - b); the swap chain runs on one thread over the
+// position permutation staged in SMEM (global memory when C does not fit).
+constexpr uint32_t FIRO_SMEM_SLOTS = 48 * 1024;
+__global__ void __launch_bounds__(SAMPLE_THREADS, 1)
+firo_sample_kernel(ResArgs a, int32_t* slots, uint32_t B) {
+  extern __shared__ uint32_t s_pos[];
+  ResDev* st = a.st;
+  const uint32_t p = st->p;
+  const uint64_t d = st->d;
+  const uint32_t need = st->over ? 1u : a.theta + B;
+  const uint32_t n = p >= need ? (p < B ? p : B) : 0u;
+  const bool in_smem = a.C <= FIRO_SMEM_SLOTS;
+  uint32_t* pos = in_smem ? s_pos : a.pos;
+  if (in_smem)
+    for (uint32_t i = threadIdx.x; i < a.C; i += blockDim.x) s_pos[i] = a.pos[i];
+  for (uint32_t b = threadIdx.x; b < n; b += blockDim.x)
+    slots[b] = (int32_t)bounded(philox_r64(a.seed, TAG_DRAIN, d + b, a.rank), p - b);   // k_b, for now
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t b = 0; b < n; ++b) {
+      const uint32_t k = (uint32_t)slots[b], last = p - 1 - b;
+      const uint32_t j = pos[k];
+      pos[k] = pos[last];
+      pos[last] = j;
+      slots[b] = (int32_t)j;
+    }
+  }
+  __syncthreads();
+  for (uint32_t b = threadIdx.x; b < n; b += blockDim.x) a.seen[slots[b]] = 1;
+  if (in_smem)
+    for (uint32_t i = threadIdx.x; i < a.C; i += blockDim.x) a.pos[i] = s_pos[i];
+  if (threadIdx.x == 0) finish_queue_batch(a, p, n, d + n);
+}
+
 __global__ void __launch_bounds__(SAMPLE_THREADS, 1)
 sample_kernel(ResArgs a, int32_t* slots, uint32_t B) {
   __shared__ uint32_t s_cnt;
@@ -272,7 +374,15 @@ void launch_commit(const ResArgs& a, uint64_t tail, uint32_t closed, uint32_t ma
 }
 
 void launch_sample(const ResArgs& a, int32_t* slots, uint32_t B, cudaStream_t s) {
-  sample_kernel<<<1, SAMPLE_THREADS, 0, s>>>(a, slots, B);
+  if (a.policy == 1) {
+    fifo_sample_kernel<<<1, SAMPLE_THREADS, 0, s>>>(a, slots, B);
+  } else if (a.policy == 2) {
+    const size_t smem = a.C <= FIRO_SMEM_SLOTS ? (size_t)a.C * 4 : 0;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(firo_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    firo_sample_kernel<<<1, SAMPLE_THREADS, smem, s>>>(a, slots, B);
+  } else {
+    sample_kernel<<<1, SAMPLE_THREADS, 0, s>>>(a, slots, B);
+  }
 }
 
 void launch_gather(const ResArgs& a, const int32_t* slots, uint32_t B, uint32_t tau, float* xn, cudaStream_t s) {

@@ -24,7 +24,8 @@ FLAG_NCCL_EXCHANGE = 16
 K_COMMIT, K_SAMPLE, K_GATHER, K_HEAD_FWD, K_OUT_FWD_DW, K_OUT_DH, K_HEAD_BWD, K_ALLREDUCE, K_ADAM, K_LOSS = range(10)
 KERNEL_NAMES = ["commit", "sample", "gather", "head_fwd", "out_fwd_dw", "out_dh", "head_bwd", "allreduce",
                 "adam", "loss"]
-ABI_VERSION = 1
+ABI_VERSION = 2
+RESERVOIR, FIFO, FIRO = 0, 1, 2
 
 EXPORTS = ["mel_config_default", "mel_nccl_unique_id", "mel_create", "mel_destroy", "mel_last_error",
            "mel_param_layout", "mel_set_params", "mel_get_params", "mel_get_state", "mel_set_state",
@@ -45,7 +46,8 @@ class _Config(C.Structure):
                 ("steps_per_sim", C.c_uint32), ("temp_lo", C.c_float), ("temp_hi", C.c_float),
                 ("precision", C.c_uint32), ("storage", C.c_uint32), ("lr0", C.c_double), ("lr_min", C.c_double),
                 ("lr_halving_samples", C.c_uint64), ("beta1", C.c_double), ("beta2", C.c_double),
-                ("eps", C.c_double), ("seed", C.c_uint64), ("staging_entries", C.c_uint32), ("flags", C.c_uint32)]
+                ("eps", C.c_double), ("seed", C.c_uint64), ("staging_entries", C.c_uint32), ("flags", C.c_uint32),
+                ("policy", C.c_uint32), ("pad", C.c_uint32)]
 
 
 class _Stats(C.Structure):
@@ -127,6 +129,7 @@ class Config:
     seed: int = 1
     staging_entries: int = 16
     flags: int = 0
+    policy: int = RESERVOIR
 
     def to_c(self) -> _Config:
         c = _Config()
@@ -135,7 +138,8 @@ class Config:
         h = list(self.hidden) + [0, 0]
         c.hidden[0], c.hidden[1] = h[0], h[1]
         for k in ("capacity", "threshold", "batch", "steps_per_sim", "temp_lo", "temp_hi", "precision", "storage",
-                  "lr0", "lr_min", "lr_halving_samples", "beta1", "beta2", "eps", "seed", "staging_entries", "flags"):
+                  "lr0", "lr_min", "lr_halving_samples", "beta1", "beta2", "eps", "seed", "staging_entries", "flags",
+                  "policy"):
             setattr(c, k, getattr(self, k))
         return c
 

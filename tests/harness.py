@@ -36,13 +36,13 @@ class FieldTable:
         return self.X[s]
 
 
-def make_config(wl: design.Workload, precision=0, storage=0, seed=1, staging=None, flags=0, batch=None):
+def make_config(wl: design.Workload, precision=0, storage=0, seed=1, staging=None, flags=0, batch=None, policy=0):
     # the op-log holds puts_per_step puts pending between commit points
     staging = staging or wl.puts_per_step + 8
     from paper_2309_16743_b200 import mel
     return mel.Config(n_field=wl.n_field, hidden=wl.hidden, capacity=wl.capacity, threshold=wl.threshold,
                       batch=batch or wl.batch, steps_per_sim=wl.tau, precision=precision, storage=storage,
-                      seed=seed, staging_entries=staging, flags=flags)
+                      seed=seed, staging_entries=staging, flags=flags, policy=policy)
 
 
 def tensors_f64(st):
@@ -57,10 +57,10 @@ def rel_norm(a, b):
 
 
 def replay_parity(ctx, wl, table, ops, storage=0, seed=1, reanchor=True, max_train_steps=None,
-                  on_step=None, check_every_sample=True):
+                  on_step=None, check_every_sample=True, policy=0):
     """Drive ctx (world 1) and an oracle reservoir with the same op-log.  Returns a
     report dict; asserts bit-exact sampling on the way."""
-    res = ores.Reservoir(wl.capacity, wl.threshold, wl.n_field, seed=seed, rank=0, storage=storage)
+    res = ores.Reservoir(wl.capacity, wl.threshold, wl.n_field, seed=seed, rank=0, storage=storage, policy=policy)
     report = dict(loss_err=[], w_err=[], steps=0, samples=0, eagain=0)
     last_slots = []
     S_host = 0

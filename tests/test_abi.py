@@ -47,7 +47,7 @@ def test_config_default_without_gpu(lib):
     from paper_2309_16743_b200 import mel
     c = mel._Config()
     assert lib.mel_config_default(ctypes.byref(c), 1000000, 1024) == 0
-    assert c.abi_version == 1 and c.capacity == 6000 and c.threshold == 1000
+    assert c.abi_version == 2 and c.capacity == 6000 and c.threshold == 1000 and c.policy == 0
     assert list(c.hidden) == [256, 256] and c.lr0 == 1e-3 and c.lr_min == 2.5e-4
     assert c.temp_lo == 100.0 and c.temp_hi == 500.0 and c.lr_halving_samples == 10000
 
