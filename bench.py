@@ -298,7 +298,7 @@ def main():
             tl2 = allc[160 * 32 + 768:].reshape(17, 8).astype(np.int64)
             names = {0: "mma_total", 1: "mma_w_full", 2: "mma_h_full", 3: "mma_y_empty", 4: "mma_dy_full",
                      5: "mma_dw_empty", 6: "mma_fwd_issue", 7: "mma_dw_issue", 8: "epi_total", 9: "epi_t_full", 10: "epi_y_full", 11: "epi_dy_empty",
-                     12: "epi_store_bar", 13: "epi_dw_readout", 14: "epi_db_bar", 16: "tma_total", 17: "tma_w_empty",
+                     12: "epi_adam_load_wait", 13: "epi_dw_readout", 14: "epi_db_bar", 16: "tma_total", 17: "tma_w_empty",
                      18: "tma_h_empty", 24: "ld_total", 25: "ld_t_empty"}
             k1 = {v: float(prof[:, k].mean()) for k, v in names.items()}
             print(json.dumps({"ms_per_step": ms_step, "value": value, "k1_wait_cycles_mean_per_cta": k1}), flush=True)

@@ -12,6 +12,9 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmel.so")
+# A/B comparisons of two builds (tools/ab_bench.sh): MEL_LIB names another in-tree build
+if os.environ.get("MEL_LIB"):
+    LIB_PATH = os.path.join(os.path.dirname(LIB_PATH), os.path.basename(os.environ["MEL_LIB"]))
 
 OK, EAGAIN, EOS = 0, 1, 2
 EINVAL, ECLOSED, EPROTO, ECUDA, ENCCL, ENOMEM, ENONFINITE = -1, -2, -3, -4, -5, -6, -7
