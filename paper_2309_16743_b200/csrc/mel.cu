@@ -237,6 +237,8 @@ int validate(const mel_config* g, int world, mel_ctx* c) {
   if (g->precision > MEL_BF16 || g->storage > MEL_STORE_BF16) return fail(c, MEL_EINVAL, "bad precision/storage");
   if (g->staging_entries == 0) return fail(c, MEL_EINVAL, "staging_entries must be >= 1");
   if (g->policy > MEL_FIRO) return fail(c, MEL_EINVAL, "unknown buffer policy %u", g->policy);
+  if (!(g->eps > 0.0) || !(g->beta1 >= 0.0 && g->beta1 < 1.0) || !(g->beta2 >= 0.0 && g->beta2 < 1.0))
+    return fail(c, MEL_EINVAL, "Adam needs eps > 0 and 0 <= beta < 1");
   if (g->policy == MEL_FIFO && g->batch > g->capacity) return fail(c, MEL_EINVAL, "FIFO needs batch <= capacity");
   if (g->policy == MEL_FIRO && (uint64_t)g->threshold + g->batch > g->capacity)
     return fail(c, MEL_EINVAL, "FIRO needs threshold + batch <= capacity");
