@@ -213,6 +213,13 @@ int reservoir_sample_batch(mel_ctx* ctx, int32_t* slots_host, uint32_t* n_host);
  * rank closed and drained), MEL_ENONFINITE (loss not finite), errors. */
 int surrogate_step(mel_ctx* ctx, double* loss_host);
 
+/* Result of an earlier surrogate_step call without draining the stream: `call` is the
+ * 0-based index of that call on this context, one of the last 16.  Waits only until that
+ * step's kernels have finished (so a producer loop can read step i-1's loss while step i
+ * runs), then returns its global mean loss (loss_host) and status (status_host: 0 trained,
+ * 1 no rank had samples).  MEL_EINVAL for a call index out of range. */
+int surrogate_step_result(mel_ctx* ctx, uint64_t call, double* loss_host, int* status_host);
+
 /* Forward-only validation of n samples given on the host: X_host n x 5
  * kelvin, t_host n, fields_host n x N fp32 kelvin (nullable: then no MSE).
  * mse_host (nullable) receives the MSE in normalised units (reading Q13);

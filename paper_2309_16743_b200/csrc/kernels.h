@@ -33,7 +33,12 @@ struct Mirror {
   double n_total;
   int32_t status;      // step: 0 ok, 1 skip (no samples)
   uint32_t pad;
+  // per-call results of the last MEL_RESULT_RING surrogate_step calls (slot = call % ring),
+  // read by surrogate_step_result without draining the stream
+  double ring_loss[16];
+  int32_t ring_status[16];
 };
+constexpr int MEL_RESULT_RING = 16;
 
 struct StMeta {        // staging-ring metadata (32 B)
   uint32_t sim, t;
@@ -105,7 +110,7 @@ int out_fwd_f32(const OutArgs& a, cudaStream_t s);   // returns number of partia
 void col_sum(const float* X, int rows, int cols, int ld, float* out, cudaStream_t s);
 void reduce_local(StepDev* sd, const double* parts, int n_parts, const ResDev* st, cudaStream_t s);
 void step_finalize(StepDev* sd, double n_field, double lr0, double lr_min, uint64_t halving, double b1, double b2,
-                   Mirror* mirror, ResDev* st, cudaStream_t s);
+                   Mirror* mirror, ResDev* st, cudaStream_t s, uint32_t slot = 0);
 void step_prepare(StepDev* sd, const ResDev* st, double n_field, double lr0, double lr_min, uint64_t halving, double b1,
                   double b2, cudaStream_t s, bool global_n = false);   // global_n: use sd->n_glob
 void stage_count(StepDev* sd, const ResDev* st, cudaStream_t s);     // sd->n_glob = st->n_last

@@ -55,6 +55,8 @@ struct mel_ctx {
   uint64_t known_consumed = 0;
   bool copy_fence = false;                  // see ensure_ring_space
   uint64_t drawn = 0;                       // items handed out (FIFO / FIRO remove them)
+  uint64_t calls = 0;                       // surrogate_step calls (surrogate_step_result)
+  cudaEvent_t ev_call[MEL_RESULT_RING] = {};
   bool closed = false;
   bool copy_pending = false;
   cudaEvent_t ev_copy = nullptr, ev_fence = nullptr;
@@ -646,6 +648,7 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
   CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_fence, cudaEventDisableTiming));
+  for (int i = 0; i < MEL_RESULT_RING; ++i) CK(cudaEventCreateWithFlags(&c->ev_call[i], cudaEventDisableTiming));
 
   // geometry: dims = [6, hidden..., N]
   c->dims[0] = 6;
@@ -855,6 +858,8 @@ void mel_destroy(mel_ctx* c) {
   if (c->h_stmeta) cudaFreeHost(c->h_stmeta);
   if (c->ev_copy) cudaEventDestroy(c->ev_copy);
   if (c->ev_fence) cudaEventDestroy(c->ev_fence);
+  for (int i = 0; i < MEL_RESULT_RING; ++i)
+    if (c->ev_call[i]) cudaEventDestroy(c->ev_call[i]);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -1062,7 +1067,7 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
   {
     Timer t(c, MEL_K_LOSS, 1);
     step_finalize(c->d_sd, (double)c->N, c->cfg.lr0, c->cfg.lr_min, c->cfg.lr_halving_samples, c->cfg.beta1,
-                  c->cfg.beta2, c->d_mirror, c->d_st, c->stream);
+                  c->cfg.beta2, c->d_mirror, c->d_st, c->stream, (uint32_t)(c->calls % MEL_RESULT_RING));
   }
   if (c->fused_adam || c->peer) {
     // W_L was updated inside K1 (new shadow in the other buffer, written to every rank in
@@ -1108,6 +1113,8 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
     c->ag_pending = true;
   }
   if ((r = check_launch(c, "adam"))) return r;
+  CK(cudaEventRecord(c->ev_call[c->calls % MEL_RESULT_RING], c->stream));
+  c->calls += 1;
   c->batch_known = false;
   const bool need_sync = loss_host || !local_has || c->closed;
   if (!need_sync) return MEL_OK;
@@ -1132,6 +1139,19 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
   }
   if (loss_host) *loss_host = m.loss;
   if (!std::isfinite(m.loss)) return fail(c, MEL_ENONFINITE, "loss is not finite (%g)", m.loss);
+  return MEL_OK;
+}
+
+int surrogate_step_result(mel_ctx* c, uint64_t call, double* loss_host, int* status_host) {
+  GUARD(c);
+  if (call >= c->calls || c->calls - call > (uint64_t)MEL_RESULT_RING)
+    return fail(c, MEL_EINVAL, "step call %llu not among the last %d calls", (unsigned long long)call,
+                MEL_RESULT_RING);
+  const int slot = (int)(call % MEL_RESULT_RING);
+  CK(cudaEventSynchronize(c->ev_call[slot]));               // that step only, not the stream
+  const volatile Mirror* m = c->h_mirror;
+  if (loss_host) *loss_host = m->ring_loss[slot];
+  if (status_host) *status_host = m->ring_status[slot];
   return MEL_OK;
 }
 

@@ -208,13 +208,14 @@ __global__ void reduce_local_kernel(StepDev* sd, const double* parts, int n_part
 }
 
 __global__ void step_finalize_kernel(StepDev* sd, double n_field, double lr0, double lr_min, uint64_t halving,
-                                     double b1, double b2, Mirror* mirror, ResDev* st) {
+                                     double b1, double b2, Mirror* mirror, ResDev* st, uint32_t slot) {
   const double sse = sd->red[0], n = sd->red[1];
   st->n_last = 0;                       // a batch is consumed by exactly one step
   mirror->n_last = 0;
   if (n <= 0.0) {
     sd->skip = 1;
     mirror->status = 1; mirror->n_total = 0.0;
+    mirror->ring_status[slot] = 1; mirror->ring_loss[slot] = 0.0;
     return;
   }
   sd->skip = 0;
@@ -232,6 +233,7 @@ __global__ void step_finalize_kernel(StepDev* sd, double n_field, double lr0, do
   sd->k = k;
   sd->S = S + (uint64_t)n;
   mirror->status = 0; mirror->loss = sd->loss; mirror->n_total = n;
+  mirror->ring_status[slot] = 0; mirror->ring_loss[slot] = sd->loss;
   mirror->adam_k = k; mirror->samples = sd->S;
 }
 
@@ -432,8 +434,8 @@ void reduce_local(StepDev* sd, const double* parts, int n_parts, const ResDev* s
 }
 
 void step_finalize(StepDev* sd, double n_field, double lr0, double lr_min, uint64_t halving, double b1, double b2,
-                   Mirror* mirror, ResDev* st, cudaStream_t s) {
-  step_finalize_kernel<<<1, 1, 0, s>>>(sd, n_field, lr0, lr_min, halving, b1, b2, mirror, st);
+                   Mirror* mirror, ResDev* st, cudaStream_t s, uint32_t slot) {
+  step_finalize_kernel<<<1, 1, 0, s>>>(sd, n_field, lr0, lr_min, halving, b1, b2, mirror, st, slot);
 }
 
 void step_prepare(StepDev* sd, const ResDev* st, double n_field, double lr0, double lr_min, uint64_t halving, double b1,

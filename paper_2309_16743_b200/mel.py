@@ -32,7 +32,8 @@ RESERVOIR, FIFO, FIRO = 0, 1, 2
 
 EXPORTS = ["mel_config_default", "mel_nccl_unique_id", "mel_create", "mel_destroy", "mel_last_error",
            "mel_param_layout", "mel_set_params", "mel_get_params", "mel_get_state", "mel_set_state",
-           "reservoir_put", "reservoir_close", "reservoir_sample_batch", "surrogate_step", "surrogate_eval",
+           "reservoir_put", "reservoir_close", "reservoir_sample_batch", "surrogate_step", "surrogate_step_result",
+           "surrogate_eval",
            "reservoir_stats", "reservoir_dump", "mel_sync", "mel_kernel_time", "mel_kernel_time_reset",
            "mel_launch_count", "mel_set_flags", "mel_debug_counters"]
 
@@ -92,6 +93,7 @@ def load_library(path: str = LIB_PATH):
         "reservoir_close": (C.c_int, [vp]),
         "reservoir_sample_batch": (C.c_int, [vp, C.POINTER(i32), C.POINTER(u32)]),
         "surrogate_step": (C.c_int, [vp, C.POINTER(C.c_double)]),
+        "surrogate_step_result": (C.c_int, [vp, u64, C.POINTER(C.c_double), C.POINTER(C.c_int)]),
         "surrogate_eval": (C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(u32), C.POINTER(C.c_float), u32,
                                      C.POINTER(C.c_double), C.POINTER(C.c_float)]),
         "reservoir_stats": (C.c_int, [vp, C.POINTER(_Stats)]),
@@ -229,7 +231,15 @@ class Context:
         loss = C.c_double()
         r = self.lib.surrogate_step(self.h, C.byref(loss) if want_loss else None)
         self._check(r, (OK, EAGAIN, EOS))
+        self.step_calls = getattr(self, "step_calls", 0) + 1
         return r, (loss.value if (want_loss and r == OK) else None)
+
+    def step_result(self, call: int):
+        """(status, loss) of the call-th step() (0-based, one of the last 16), waiting
+        only for that step's kernels."""
+        loss, st = C.c_double(), C.c_int()
+        self._check(self.lib.surrogate_step_result(self.h, call, C.byref(loss), C.byref(st)))
+        return st.value, loss.value
 
     def eval(self, X, t, fields=None, want_pred=False):
         X = np.ascontiguousarray(X, dtype=np.float32)

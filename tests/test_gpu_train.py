@@ -159,3 +159,36 @@ def test_invalid_configurations_fail_loudly(mel):
         with pytest.raises(mel.MelError) as e:
             mel.Context(cfg)
         assert e.value.code == mel.EINVAL
+
+
+def test_step_result_matches_synchronous_loss(mel):
+    """surrogate_step_result(i) returns the same loss as the synchronous
+    surrogate_step(loss) of that call, for the last 16 calls, without a stream drain."""
+    wl = _bf16_wl(n=40, batch=128, capacity=400, threshold=50, sims=30, puts_per_step=40)
+    table = FieldTable(wl)
+    a = mel.Context(make_config(wl, precision=1, storage=1))
+    b = mel.Context(make_config(wl, precision=1, storage=1))
+    sync_losses, calls = [], 0
+    for op in design.build_oplog(wl):
+        if op[0] == "PUT":
+            _, r, s, t = op
+            a.put(s, t, table.Xs(s), table.field(s, t)); b.put(s, t, table.Xs(s), table.field(s, t))
+        elif op[0] == "SAMPLE":
+            a.sample(); b.sample()
+        elif op[0] == "STEP":
+            st_a, la = a.step(want_loss=True)
+            st_b, _ = b.step(want_loss=False)
+            sync_losses.append((st_a, la))
+            calls += 1
+            if calls == 20:
+                break
+    for i in range(calls - 16, calls):
+        st, loss = b.step_result(i)
+        st_a, la = sync_losses[i]
+        assert st == (0 if st_a == 0 else 1)
+        if st_a == 0:
+            assert loss == la
+    with pytest.raises(mel.MelError):
+        b.step_result(calls - 17)
+    with pytest.raises(mel.MelError):
+        b.step_result(calls)
