@@ -688,9 +688,12 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
   CK(cudaHostAlloc((void**)&c->h_mirror, sizeof(Mirror), cudaHostAllocMapped));
   memset(c->h_mirror, 0, sizeof(Mirror));
   CK(cudaHostGetDevicePointer((void**)&c->d_mirror, c->h_mirror, 0));
-  CK(cudaHostAlloc((void**)&c->h_stmeta, sizeof(StMeta) * S, cudaHostAllocDefault));
+  // staging metadata lives in mapped pinned memory: the commit kernel reads the 32-byte
+  // entries straight from the host (no per-put copy on the stream)
+  CK(cudaHostAlloc((void**)&c->h_stmeta, sizeof(StMeta) * S, cudaHostAllocMapped));
+  memset(c->h_stmeta, 0, sizeof(StMeta) * S);
   StMeta* d_stmeta; float* d_stfield;
-  DALLOC(d_stmeta, S);
+  CK(cudaHostGetDevicePointer((void**)&d_stmeta, c->h_stmeta, 0));
   DALLOC(d_stfield, (size_t)S * c->Npad);
   CK(cudaMemset(d_stfield, 0, sizeof(float) * (size_t)S * c->Npad));
   DALLOC(a.meta, C);
@@ -845,7 +848,7 @@ void mel_destroy(mel_ctx* c) {
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   drain_timers(c);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
-  void* ptrs[] = {c->d_st, (void*)c->ra.st_meta, (void*)c->ra.st_field, c->ra.meta, c->ra.seen, c->ra.put_seq,
+  void* ptrs[] = {c->d_st, (void*)c->ra.st_field, c->ra.meta, c->ra.seen, c->ra.put_seq,
                   c->ra.bitmap, c->ra.pos, c->ra.payload, c->ra.plan, c->d_slots, c->d_p, c->d_m, c->d_v, c->d_g,
                   c->d_shadow[0], c->d_shadow[1], c->d_xn, c->d_z[0], c->d_z[1], c->d_h[0], c->d_h[1], c->d_dz[0],
                   c->d_dz[1], c->d_dy, c->d_part, c->d_sse_part, c->d_sd, c->d_eval_x, c->d_eval_t, c->d_eval_y,
@@ -969,13 +972,11 @@ int reservoir_put(mel_ctx* c, uint32_t sim, uint32_t t, const float X[5], const 
   StMeta m{};
   m.sim = sim; m.t = t;
   for (int i = 0; i < 5; ++i) m.X[i] = X[i];
-  // the pinned metadata mirror entry may still be read by an earlier async copy
-  // of the same entry only if the ring wrapped, which ensure_ring_space excluded
+  // the mapped metadata entry is read by the commit kernel that consumes it; it is only
+  // rewritten after that commit published its progress (ensure_ring_space)
   c->h_stmeta[e] = m;
   float* dst = const_cast<float*>(c->ra.st_field) + (uint64_t)e * c->Npad;
-  StMeta* dmeta = const_cast<StMeta*>(c->ra.st_meta) + e;
   if (on_device) {
-    CK(cudaMemcpyAsync(dmeta, &c->h_stmeta[e], sizeof(StMeta), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(dst, field, 4ull * c->N, cudaMemcpyDeviceToDevice, c->stream));
   } else {
     if (c->copy_fence) {
@@ -983,7 +984,6 @@ int reservoir_put(mel_ctx* c, uint32_t sim, uint32_t t, const float X[5], const 
       CK(cudaStreamWaitEvent(c->copy_stream, c->ev_fence, 0));
       c->copy_fence = false;
     }
-    CK(cudaMemcpyAsync(dmeta, &c->h_stmeta[e], sizeof(StMeta), cudaMemcpyHostToDevice, c->copy_stream));
     CK(cudaMemcpyAsync(dst, field, 4ull * c->N, cudaMemcpyHostToDevice, c->copy_stream));
     CK(cudaEventRecord(c->ev_copy, c->copy_stream));
     c->copy_pending = true;
