@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <utility>
 
 namespace mel {
 
@@ -61,3 +62,29 @@ __device__ __forceinline__ float bf16_bits_to_f32(uint16_t h) {
 }
 
 }  // namespace mel
+
+// Programmatic dependent launch: every library kernel starts with pdl_enter() -- wait for
+// the preceding kernel in the stream to complete (its writes visible), then let the next
+// kernel's CTAs be scheduled on SMs as this grid's last CTAs retire -- and is launched with
+// launch_pdl, so a kernel's launch and prologue overlap its predecessor's tail without
+// changing stream semantics (griddepcontrol.wait is a no-op without the attribute).
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}

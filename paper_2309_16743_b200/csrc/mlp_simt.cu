@@ -19,6 +19,7 @@ __global__ void __launch_bounds__(256)
 sgemm_kernel(int M, int N, int K, const float* __restrict__ A, int lda, const float* __restrict__ B, int ldb,
              float* __restrict__ C, int ldc, int epi, const float* __restrict__ bias, float* __restrict__ H, int ldh,
              int k_chunk) {
+  pdl_enter();
   __shared__ float As[TK][TM + 4];
   __shared__ float Bs[TK][TN + 4];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -78,6 +79,7 @@ sgemm_kernel(int M, int N, int K, const float* __restrict__ A, int lda, const fl
 
 __global__ void splitk_reduce_kernel(int M, int N, int splits, const float* __restrict__ part, float* __restrict__ C,
                                      int ldc, const float* __restrict__ mask, int ldm) {
+  pdl_enter();
   const size_t total = (size_t)M * N;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
     const int m = (int)(i / N), n = (int)(i % N);
@@ -92,6 +94,7 @@ __global__ void splitk_reduce_kernel(int M, int N, int splits, const float* __re
 // for valid rows/cols (0 elsewhere), SSE partial per block.
 __global__ void __launch_bounds__(256)
 out_fwd_f32_kernel(OutArgs a) {
+  pdl_enter();
   __shared__ float As[TK][TM + 4];
   __shared__ float Bs[TK][TN + 4];
   __shared__ double s_red[256];
@@ -162,6 +165,7 @@ out_fwd_f32_kernel(OutArgs a) {
 // fixed strided order, then the 8 partials in fixed order (deterministic)
 __global__ void __launch_bounds__(256)
 col_sum_kernel(const float* __restrict__ X, int rows, int cols, int ld, float* __restrict__ out) {
+  pdl_enter();
   __shared__ float part[8][33];
   const int cl = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + cl;
@@ -183,6 +187,7 @@ col_sum_kernel(const float* __restrict__ X, int rows, int cols, int ld, float* _
 __global__ void splitk_reduce_epi_kernel(int M, int N, int splits, const float* __restrict__ part, float* __restrict__ C,
                                          int ldc, int epi, const float* __restrict__ bias, float* __restrict__ H,
                                          int ldh) {
+  pdl_enter();
   const size_t total = (size_t)M * N;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
     const int m = (int)(i / N), n = (int)(i % N);
@@ -195,6 +200,7 @@ __global__ void splitk_reduce_epi_kernel(int M, int N, int splits, const float* 
 }
 
 __global__ void reduce_local_kernel(StepDev* sd, const double* parts, int n_parts, const ResDev* st) {
+  pdl_enter();
   __shared__ double s[256];
   double v = 0.0;
   for (int i = threadIdx.x; i < n_parts; i += 256) v += parts[i];
@@ -209,6 +215,7 @@ __global__ void reduce_local_kernel(StepDev* sd, const double* parts, int n_part
 
 __global__ void step_finalize_kernel(StepDev* sd, double n_field, double lr0, double lr_min, uint64_t halving,
                                      double b1, double b2, Mirror* mirror, ResDev* st, uint32_t slot) {
+  pdl_enter();
   const double sse = sd->red[0], n = sd->red[1];
   st->n_last = 0;                       // a batch is consumed by exactly one step
   mirror->n_last = 0;
@@ -241,6 +248,7 @@ __global__ void step_finalize_kernel(StepDev* sd, double n_field, double lr0, do
 // values step_finalize computes afterwards (scale, lr, bias corrections of step k+1).
 __global__ void step_prepare_kernel(StepDev* sd, const ResDev* st, double n_field, double lr0, double lr_min,
                                     uint64_t halving, double b1, double b2, int global_n) {
+  pdl_enter();
   const double n = global_n ? sd->n_glob : (double)st->n_last;
   if (n <= 0.0) { sd->skip = 1; return; }
   sd->skip = 0;
@@ -293,6 +301,7 @@ __global__ void __launch_bounds__(256)
 adam_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v, const float* __restrict__ g,
             uint64_t n4, const StepDev* __restrict__ sd, float b1, float b2, float eps,
             __nv_bfloat16* __restrict__ shadow, uint64_t sh_begin, uint64_t sh_end) {
+  pdl_enter();
   if (sd->skip) return;
   const float scale = sd->scale, step = sd->lr / sd->c1, isc2 = rsqrtf(sd->c2);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -326,6 +335,7 @@ adam_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
 }
 
 __global__ void init_kernel(float* dst, uint64_t count, uint32_t tid, uint32_t fan_in, uint64_t seed) {
+  pdl_enter();
   const double a = 1.0 / sqrt((double)fan_in);
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
     const double u = unit_double(philox_r64(seed, TAG_INIT, i, tid));
@@ -334,17 +344,20 @@ __global__ void init_kernel(float* dst, uint64_t count, uint32_t tid, uint32_t f
 }
 
 __global__ void to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, uint64_t n) {
+  pdl_enter();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     dst[i] = __float2bfloat16_rn(src[i]);
 }
 
 __global__ void relu_mask_kernel(float* X, const float* Z, uint64_t n) {
+  pdl_enter();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     if (!(Z[i] > 0.f)) X[i] = 0.f;
 }
 
 __global__ void eval_mse_kernel(const float* __restrict__ Y, const float* __restrict__ T, int rows, int cols, int ld,
                                 double* part) {
+  pdl_enter();
   __shared__ double s[256];
   double acc = 0.0;
   const size_t total = (size_t)rows * cols;
@@ -364,6 +377,7 @@ __global__ void eval_mse_kernel(const float* __restrict__ Y, const float* __rest
 
 __global__ void eval_inputs_kernel(const float* X, const uint32_t* t, int n, uint32_t tau, float lo, float span,
                                    float* xn) {
+  pdl_enter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= n) return;
   float o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -373,6 +387,7 @@ __global__ void eval_inputs_kernel(const float* X, const uint32_t* t, int n, uin
 }
 
 __global__ void normalise_kernel(const float* src, float* dst, uint64_t n, float lo, float span) {
+  pdl_enter();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     dst[i] = normalise_rn(src[i], lo, span);
 }
@@ -392,25 +407,25 @@ void sgemm(bool ta, bool tb, int M, int N, int K, const float* A, int lda, const
   int k_chunk = (K + splits - 1) / splits;
   k_chunk = ((k_chunk + TK - 1) / TK) * TK;
   dim3 grid((N + TN - 1) / TN, (M + TM - 1) / TM, splits);
-  if (!ta && !tb) sgemm_kernel<false, false><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk);
-  else if (!ta && tb) sgemm_kernel<false, true><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk);
-  else if (ta && !tb) sgemm_kernel<true, false><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk);
-  else sgemm_kernel<true, true><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk);
+  if (!ta && !tb) launch_pdl(sgemm_kernel<false, false>, dim3(grid), dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk);
+  else if (!ta && tb) launch_pdl(sgemm_kernel<false, true>, dim3(grid), dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk);
+  else if (ta && !tb) launch_pdl(sgemm_kernel<true, false>, dim3(grid), dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk);
+  else launch_pdl(sgemm_kernel<true, true>, dim3(grid), dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk);
 }
 
 void splitk_reduce(int M, int N, int splits, const float* part, float* C, int ldc, const float* relu_mask, int ldm,
                    cudaStream_t s) {
-  splitk_reduce_kernel<<<grid_for((uint64_t)M * N), 256, 0, s>>>(M, N, splits, part, C, ldc, relu_mask, ldm);
+  launch_pdl(splitk_reduce_kernel, dim3(grid_for((uint64_t)M * N)), dim3(256), 0, s, M, N, splits, part, C, ldc, relu_mask, ldm);
 }
 
 int out_fwd_f32(const OutArgs& a, cudaStream_t s) {
   dim3 grid((unsigned)((a.Npad + TN - 1) / TN), (a.B + TM - 1) / TM);
-  out_fwd_f32_kernel<<<grid, 256, 0, s>>>(a);
+  launch_pdl(out_fwd_f32_kernel, dim3(grid), dim3(256), 0, s, a);
   return (int)(grid.x * grid.y);
 }
 
 void col_sum(const float* X, int rows, int cols, int ld, float* out, cudaStream_t s) {
-  col_sum_kernel<<<(cols + 31) / 32, 256, 0, s>>>(X, rows, cols, ld, out);
+  launch_pdl(col_sum_kernel, dim3((cols + 31) / 32), dim3(256), 0, s, X, rows, cols, ld, out);
 }
 
 // SIMT GEMM that fills the GPU: split-K through `scratch` (>= splits*M*N floats) when
@@ -425,59 +440,60 @@ int sgemm_auto(bool ta, bool tb, int M, int N, int K, const float* A, int lda, c
     return 1;
   }
   sgemm(ta, tb, M, N, K, A, lda, B, ldb, scratch, N, EPI_STORE, nullptr, nullptr, 0, sk, s);
-  splitk_reduce_epi_kernel<<<grid_for((uint64_t)M * N), 256, 0, s>>>(M, N, sk, scratch, C, ldc, epi, bias, H, ldh);
+  launch_pdl(splitk_reduce_epi_kernel, dim3(grid_for((uint64_t)M * N)), dim3(256), 0, s, M, N, sk, scratch, C, ldc, epi, bias, H, ldh);
   return 2;
 }
 
 void reduce_local(StepDev* sd, const double* parts, int n_parts, const ResDev* st, cudaStream_t s) {
-  reduce_local_kernel<<<1, 256, 0, s>>>(sd, parts, n_parts, st);
+  launch_pdl(reduce_local_kernel, dim3(1), dim3(256), 0, s, sd, parts, n_parts, st);
 }
 
 void step_finalize(StepDev* sd, double n_field, double lr0, double lr_min, uint64_t halving, double b1, double b2,
                    Mirror* mirror, ResDev* st, cudaStream_t s, uint32_t slot) {
-  step_finalize_kernel<<<1, 1, 0, s>>>(sd, n_field, lr0, lr_min, halving, b1, b2, mirror, st, slot);
+  launch_pdl(step_finalize_kernel, dim3(1), dim3(1), 0, s, sd, n_field, lr0, lr_min, halving, b1, b2, mirror, st, slot);
 }
 
 void step_prepare(StepDev* sd, const ResDev* st, double n_field, double lr0, double lr_min, uint64_t halving, double b1,
                   double b2, cudaStream_t s, bool global_n) {
-  step_prepare_kernel<<<1, 1, 0, s>>>(sd, st, n_field, lr0, lr_min, halving, b1, b2, global_n ? 1 : 0);
+  launch_pdl(step_prepare_kernel, dim3(1), dim3(1), 0, s, sd, st, n_field, lr0, lr_min, halving, b1, b2, global_n ? 1 : 0);
 }
 
-__global__ void stage_count_kernel(StepDev* sd, const ResDev* st) { sd->n_glob = (double)st->n_last; }
+__global__ void stage_count_kernel(StepDev* sd, const ResDev* st) {
+  pdl_enter(); sd->n_glob = (double)st->n_last; }
 
-void stage_count(StepDev* sd, const ResDev* st, cudaStream_t s) { stage_count_kernel<<<1, 1, 0, s>>>(sd, st); }
+void stage_count(StepDev* sd, const ResDev* st, cudaStream_t s) { launch_pdl(stage_count_kernel, dim3(1), dim3(1), 0, s, sd, st); }
 
 void adam_flat(float* p, float* m, float* v, const float* g, uint64_t n, const StepDev* sd, float b1, float b2,
                float eps, __nv_bfloat16* shadow, uint64_t sh_begin, uint64_t sh_end, cudaStream_t s) {
   const uint64_t n4 = n / 4;   // the flat buffer is padded to a multiple of 4
-  adam_kernel<2><<<grid_for(n4, 256, 148 * 16), 256, 0, s>>>(p, m, v, g, n4, sd, b1, b2, eps, shadow, sh_begin, sh_end);
+  launch_pdl(adam_kernel<2>, dim3(grid_for(n4, 256, 148 * 16)), dim3(256), 0, s, p, m, v, g, n4, sd, b1, b2, eps, shadow, sh_begin, sh_end);
 }
 
 void init_tensor(float* dst, uint64_t count, uint32_t tid, uint32_t fan_in, uint64_t seed, cudaStream_t s) {
-  init_kernel<<<grid_for(count), 256, 0, s>>>(dst, count, tid, fan_in, seed);
+  launch_pdl(init_kernel, dim3(grid_for(count)), dim3(256), 0, s, dst, count, tid, fan_in, seed);
 }
 
 void to_bf16(const float* src, __nv_bfloat16* dst, uint64_t n, cudaStream_t s) {
-  to_bf16_kernel<<<grid_for(n), 256, 0, s>>>(src, dst, n);
+  launch_pdl(to_bf16_kernel, dim3(grid_for(n)), dim3(256), 0, s, src, dst, n);
 }
 
 void relu_mask_mul(float* X, const float* Z, uint64_t n, cudaStream_t s) {
-  relu_mask_kernel<<<grid_for(n), 256, 0, s>>>(X, Z, n);
+  launch_pdl(relu_mask_kernel, dim3(grid_for(n)), dim3(256), 0, s, X, Z, n);
 }
 
 int eval_mse_partial(const float* Y, const float* T, int rows, int cols, int ld, double* part, cudaStream_t s) {
   const unsigned g = grid_for((uint64_t)rows * cols, 256, 256);
-  eval_mse_kernel<<<g, 256, 0, s>>>(Y, T, rows, cols, ld, part);
+  launch_pdl(eval_mse_kernel, dim3(g), dim3(256), 0, s, Y, T, rows, cols, ld, part);
   return (int)g;
 }
 
 void eval_inputs(const float* X, const uint32_t* t, int n, uint32_t tau, float lo, float span, float* xn,
                  cudaStream_t s) {
-  eval_inputs_kernel<<<(n + 127) / 128, 128, 0, s>>>(X, t, n, tau, lo, span, xn);
+  launch_pdl(eval_inputs_kernel, dim3((n + 127) / 128), dim3(128), 0, s, X, t, n, tau, lo, span, xn);
 }
 
 void normalise_fields(const float* src, float* dst, uint64_t n, float lo, float span, cudaStream_t s) {
-  normalise_kernel<<<grid_for(n), 256, 0, s>>>(src, dst, n, lo, span);
+  launch_pdl(normalise_kernel, dim3(grid_for(n)), dim3(256), 0, s, src, dst, n, lo, span);
 }
 
 }  // namespace mel

@@ -82,6 +82,7 @@ __device__ void commit_queue(const ResArgs& a, uint64_t tail, uint32_t closed) {
 
 __global__ void __launch_bounds__(CTRL_THREADS, 1)
 commit_ctrl(ResArgs a, uint64_t tail, uint32_t closed) {
+  pdl_enter();
   if (a.policy != 0) {
     commit_queue(a, tail, closed);
     return;
@@ -184,6 +185,7 @@ commit_ctrl(ResArgs a, uint64_t tail, uint32_t closed) {
 template <int STORAGE>
 __global__ void __launch_bounds__(256)
 commit_copy(ResArgs a) {
+  pdl_enter();
   const uint32_t y = blockIdx.y;
   if (y >= a.st->n_plan) return;
   const uint2 ej = a.plan[y];
@@ -224,6 +226,7 @@ __device__ __forceinline__ void finish_queue_batch(const ResArgs& a, uint32_t p,
 // FIFO: the n oldest items, n = B during reception (needs p >= B), min(B, p) after
 __global__ void __launch_bounds__(SAMPLE_THREADS, 1)
 fifo_sample_kernel(ResArgs a, int32_t* slots, uint32_t B) {
+  pdl_enter();
   ResDev* st = a.st;
   const uint32_t p = st->p, head = st->head;
   const uint32_t n = st->over ? (p < B ? p : B) : (p >= B ? B : 0u);
@@ -246,6 +249,7 @@ fifo_sample_kernel(ResArgs a, int32_t* slots, uint32_t B) {
 constexpr uint32_t FIRO_SMEM_SLOTS = 48 * 1024;
 __global__ void __launch_bounds__(SAMPLE_THREADS, 1)
 firo_sample_kernel(ResArgs a, int32_t* slots, uint32_t B) {
+  pdl_enter();
   extern __shared__ uint32_t s_pos[];
   ResDev* st = a.st;
   const uint32_t p = st->p;
@@ -277,6 +281,7 @@ firo_sample_kernel(ResArgs a, int32_t* slots, uint32_t B) {
 
 __global__ void __launch_bounds__(SAMPLE_THREADS, 1)
 sample_kernel(ResArgs a, int32_t* slots, uint32_t B) {
+  pdl_enter();
   __shared__ uint32_t s_cnt;
   ResDev* st = a.st;
   if (threadIdx.x == 0) s_cnt = 0;
@@ -329,6 +334,7 @@ sample_kernel(ResArgs a, int32_t* slots, uint32_t B) {
 }
 
 __global__ void gather_inputs(ResArgs a, const int32_t* slots, uint32_t B, uint32_t tau, float* xn) {
+  pdl_enter();
   const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const uint32_t n = a.st->n_last;
@@ -345,6 +351,7 @@ __global__ void gather_inputs(ResArgs a, const int32_t* slots, uint32_t B, uint3
 }
 
 __global__ void init_res(ResArgs a) {
+  pdl_enter();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.C; i += gridDim.x * blockDim.x) {
     a.pos[i] = i;
     a.seen[i] = 0;
@@ -363,34 +370,34 @@ void launch_commit(const ResArgs& a, uint64_t tail, uint32_t closed, uint32_t ma
   const size_t smem = (size_t)W * 4;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(commit_ctrl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  commit_ctrl<<<1, CTRL_THREADS, smem, s>>>(a, tail, closed);
+  launch_pdl(commit_ctrl, dim3(1), dim3(CTRL_THREADS), smem, s, a, tail, closed);
   if (max_entries == 0) return;
   const uint32_t n4 = (a.N + 3) / 4;
   uint32_t gx = (n4 + 255) / 256;
   if (gx > 512) gx = 512;
   dim3 grid(gx, max_entries);
-  if (a.storage == 0) commit_copy<0><<<grid, 256, 0, s>>>(a);
-  else commit_copy<1><<<grid, 256, 0, s>>>(a);
+  if (a.storage == 0) launch_pdl(commit_copy<0>, dim3(grid), dim3(256), 0, s, a);
+  else launch_pdl(commit_copy<1>, dim3(grid), dim3(256), 0, s, a);
 }
 
 void launch_sample(const ResArgs& a, int32_t* slots, uint32_t B, cudaStream_t s) {
   if (a.policy == 1) {
-    fifo_sample_kernel<<<1, SAMPLE_THREADS, 0, s>>>(a, slots, B);
+    launch_pdl(fifo_sample_kernel, dim3(1), dim3(SAMPLE_THREADS), 0, s, a, slots, B);
   } else if (a.policy == 2) {
     const size_t smem = a.C <= FIRO_SMEM_SLOTS ? (size_t)a.C * 4 : 0;
     if (smem > 48 * 1024) cudaFuncSetAttribute(firo_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    firo_sample_kernel<<<1, SAMPLE_THREADS, smem, s>>>(a, slots, B);
+    launch_pdl(firo_sample_kernel, dim3(1), dim3(SAMPLE_THREADS), smem, s, a, slots, B);
   } else {
-    sample_kernel<<<1, SAMPLE_THREADS, 0, s>>>(a, slots, B);
+    launch_pdl(sample_kernel, dim3(1), dim3(SAMPLE_THREADS), 0, s, a, slots, B);
   }
 }
 
 void launch_gather(const ResArgs& a, const int32_t* slots, uint32_t B, uint32_t tau, float* xn, cudaStream_t s) {
-  gather_inputs<<<(B + 127) / 128, 128, 0, s>>>(a, slots, B, tau, xn);
+  launch_pdl(gather_inputs, dim3((B + 127) / 128), dim3(128), 0, s, a, slots, B, tau, xn);
 }
 
 void launch_init_res(const ResArgs& a, cudaStream_t s) {
-  init_res<<<256, 256, 0, s>>>(a);
+  launch_pdl(init_res, dim3(256), dim3(256), 0, s, a);
 }
 
 }  // namespace mel
