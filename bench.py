@@ -66,8 +66,9 @@ def config_block(args, world):
             "parallelism": "dp%d" % world,
             "exchange": ("none" if world == 1 else
                          "NCCL reduce-scatter + sharded Adam + shadow all-gather" if args.flags & 16 else
-                         "in-kernel over NVLink: dW tiles TMA-stored/reduce-added into the owner rank, fused Adam at "
-                         "the owner, bf16 shadow rows pushed to every rank; NCCL for the 1.3 MB head + biases")}
+                         "in-kernel over NVLink: dW tiles (%s) TMA-stored/reduce-added into the owner rank, fused Adam "
+                         "at the owner, bf16 shadow rows pushed to every rank; NCCL for the 1.3 MB head + biases"
+                         % ("fp32" if args.flags & 32 else "bf16"))}
 
 
 # ------------------------------------------------------------------------------------
@@ -381,7 +382,8 @@ def main():
     if world > 1 and fused and dom == "out_fwd_dw":
         # bytes each rank must push over NVLink per launch: its dW of the rows other ranks own
         # (fp32) and the new bf16 shadow of its own rows to every other rank
-        nv_bytes = (world - 1) / world * n_field * K * 4.0 + (world - 1) / world * n_field * K * 2.0
+        nv_bytes = ((world - 1) / world * n_field * K * (4.0 if args.flags & mel.FLAG_FP32_EXCHANGE else 2.0) +
+                    (world - 1) / world * n_field * K * 2.0)
         nv_peak = P.get("nvlink_gbs", 770.0)
         nv_ach = nv_bytes / (kernels[dom]["ms_per_step"] / 1e3) / 1e9
         roofline["nvlink"] = {"bytes_per_launch": nv_bytes, "achieved": nv_ach, "peak": nv_peak, "unit": "GB/s",

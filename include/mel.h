@@ -114,6 +114,12 @@ typedef struct {
                                       kernel + shadow all-gather instead of the in-kernel NVLink
                                       exchange (the default when every GPU pair has peer access;
                                       DESIGN §10).  Read at mel_create only.                     */
+#define MEL_FLAG_FP32_EXCHANGE 32u /* world > 1, bf16, in-kernel exchange: dW contributions travel
+                                      over NVLink and accumulate at the owner in fp32 instead of
+                                      the default bf16 (bf16 halves the NVLink bytes: each peer
+                                      contribution is rounded once, with R > 2 the owner-side
+                                      additions round too, reading R22).  Read at
+                                      mel_create only.                                          */
 #define MEL_FLAG_NO_ZERO 2u    /* world > 1, bf16: plain all-reduce + replicated Adam instead of
                                   reduce-scatter / sharded Adam / shadow all-gather            */
 

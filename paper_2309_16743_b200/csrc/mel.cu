@@ -108,9 +108,10 @@ struct mel_ctx {
   // NVLink (CUDA IPC mappings), owners run the fused Adam and write the bf16 shadow rows to
   // every rank from inside K1; only the small region + [SSE, n] go through NCCL
   bool peer = false;
-  float* d_acc = nullptr;                   // [Npad][Klast] fp32, peers' dW sum (owned tiles' rows)
+  void* d_acc = nullptr;                    // [Npad][Klast] bf16 (fp32 with MEL_FLAG_FP32_EXCHANGE): peers' dW sum
+  bool acc_bf16 = false;
   uint32_t* d_cnt = nullptr;                // [Npad / 128] arrival counters (owned tiles)
-  float* p_acc[tc::MAX_WORLD] = {};         // every rank's acc / counters / shadows (IPC)
+  void* p_acc[tc::MAX_WORLD] = {};          // every rank's acc / counters / shadows (IPC)
   uint32_t* p_cnt[tc::MAX_WORLD] = {};
   __nv_bfloat16* p_sh[2][tc::MAX_WORLD] = {};
   uint32_t epoch = 0;
@@ -498,6 +499,7 @@ int train_step_bf16(mel_ctx* c) {
   }
   if (c->peer) {
     a.peer = 1; a.rank = (uint32_t)c->rank; a.world = (uint32_t)c->world; a.epoch = ++c->epoch;
+    a.acc_bf16 = c->acc_bf16 ? 1u : 0u;
     a.cnt_local = c->d_cnt;
     for (int q = 0; q < c->world; ++q) { a.cnt_peer[q] = c->p_cnt[q]; a.sh_peer[q] = c->p_sh[c->shadow_cur ^ 1][q]; }
   }
@@ -602,9 +604,11 @@ static int setup_peer(mel_ctx* c) {
   CK(cudaStreamSynchronize(c->stream));
   cudaFree(d_ok);
   if (!ok) return MEL_OK;
-  DALLOC(c->d_acc, rows * c->Klast);
+  c->acc_bf16 = !(c->cfg.flags & MEL_FLAG_FP32_EXCHANGE) && c->Klast % 128 == 0;
+  const size_t acc_bytes = (c->acc_bf16 ? 2 : 4) * rows * c->Klast;
+  CK(cudaMalloc(&c->d_acc, acc_bytes));
   DALLOC(c->d_cnt, tiles);
-  CK(cudaMemset(c->d_acc, 0, 4 * rows * c->Klast));
+  CK(cudaMemset(c->d_acc, 0, acc_bytes));
   CK(cudaMemset(c->d_cnt, 0, 4 * tiles));
   // handles: [acc, cnt, shadow0, shadow1] per rank
   const int NH = 4;
@@ -628,10 +632,10 @@ static int setup_peer(mel_ctx* c) {
     void* p[NH];
     for (int i = 0; i < NH; ++i)
       CK(cudaIpcOpenMemHandle(&p[i], all[(size_t)q * NH + i], cudaIpcMemLazyEnablePeerAccess));
-    c->p_acc[q] = static_cast<float*>(p[0]); c->p_cnt[q] = static_cast<uint32_t*>(p[1]);
+    c->p_acc[q] = p[0]; c->p_cnt[q] = static_cast<uint32_t*>(p[1]);
     c->p_sh[0][q] = static_cast<__nv_bfloat16*>(p[2]); c->p_sh[1][q] = static_cast<__nv_bfloat16*>(p[3]);
   }
-  if (tc::prepare_peer(c->tcb, c->Klast, rows, c->rank, c->world, c->p_acc, c->p_sh[0], c->p_sh[1]))
+  if (tc::prepare_peer(c->tcb, c->Klast, rows, c->rank, c->world, c->p_acc, c->acc_bf16, c->p_sh[0], c->p_sh[1]))
     return fail(c, MEL_ECUDA, "exchange tensor maps: %s", tc::last_error());
   c->peer = true;
   return MEL_OK;

@@ -55,6 +55,7 @@ struct OutTcArgs {
   // tiles this rank owns, the other tiles' dW are reduce-added into their owners' acc
   int peer;
   uint32_t rank, world, epoch;
+  uint32_t acc_bf16;
   uint32_t* cnt_local;
   uint32_t* cnt_peer[MAX_WORLD];
   __nv_bfloat16* sh_peer[MAX_WORLD];
@@ -62,7 +63,7 @@ struct OutTcArgs {
 
 int alloc_buffers(TcBuffers& t, uint64_t Npad, uint32_t B, uint32_t K);
 // tensor maps of the in-kernel exchange: this rank's acc and every rank's (peer-mapped) acc
-int prepare_peer(TcBuffers& t, uint32_t K, uint64_t rows, int rank, int world, float* const* acc,
+int prepare_peer(TcBuffers& t, uint32_t K, uint64_t rows, int rank, int world, void* const* acc, bool acc_bf16,
                  __nv_bfloat16* const* sh0, __nv_bfloat16* const* sh1);
 // dst = src on the rows of the tiles `rank` owns, 0 elsewhere ([Npad][K] fp32)
 void owned_rows(const TcBuffers& t, const float* src, float* dst, uint32_t K, int rank, int world, cudaStream_t s);

@@ -24,6 +24,7 @@ FLAG_TIMING = 1
 FLAG_NO_ZERO = 2
 FLAG_UNFUSED_ADAM = 8
 FLAG_NCCL_EXCHANGE = 16
+FLAG_FP32_EXCHANGE = 32
 K_COMMIT, K_SAMPLE, K_GATHER, K_HEAD_FWD, K_OUT_FWD_DW, K_OUT_DH, K_HEAD_BWD, K_ALLREDUCE, K_ADAM, K_LOSS = range(10)
 KERNEL_NAMES = ["commit", "sample", "gather", "head_fwd", "out_fwd_dw", "out_dh", "head_bwd", "allreduce",
                 "adam", "loss"]

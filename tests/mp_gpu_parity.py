@@ -32,7 +32,8 @@ def main():
 
     mode = sys.argv[1] if len(sys.argv) > 1 else "fp32"
     # bf16: in-kernel NVLink exchange (default); bf16-nccl: NCCL reduce-scatter / all-gather
-    flags = mel.FLAG_NCCL_EXCHANGE if mode.endswith("-nccl") else 0
+    flags = (mel.FLAG_NCCL_EXCHANGE if mode.endswith("-nccl") else
+             mel.FLAG_FP32_EXCHANGE if mode.endswith("-fp32x") else 0)
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(rank)
     dist.init_process_group("gloo")
