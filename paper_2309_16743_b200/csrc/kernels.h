@@ -89,11 +89,18 @@ void launch_gather(const ResArgs& a, const int32_t* slots, uint32_t B, uint32_t 
 void launch_init_res(const ResArgs& a, cudaStream_t s);
 
 // mlp_simt.cu
-enum Epi { EPI_STORE = 0, EPI_BIAS_RELU = 1, EPI_BIAS = 2 };
+enum Epi { EPI_STORE = 0, EPI_BIAS_RELU = 1, EPI_BIAS = 2, EPI_RELU_MASK = 3 };
+// optional epilogue outputs / inputs: Hb = bf16 copy of H (EPI_BIAS_RELU), mask = Z whose
+// ReLU' multiplies the result (EPI_RELU_MASK, ReLU'(0) = 0, reading R20)
+struct EpiExtra {
+  __nv_bfloat16* Hb = nullptr;
+  const float* mask = nullptr;
+  int ldm = 0;
+};
 void sgemm(bool ta, bool tb, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
-           float* C, int ldc, int epi, const float* bias, float* H, int ldh, int splits, cudaStream_t s);
+           float* C, int ldc, int epi, const float* bias, float* H, int ldh, int splits, cudaStream_t s, EpiExtra ex = EpiExtra());
 int sgemm_auto(bool ta, bool tb, int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
-               int epi, const float* bias, float* H, int ldh, float* scratch, size_t scratch_elems, cudaStream_t s);
+               int epi, const float* bias, float* H, int ldh, float* scratch, size_t scratch_elems, cudaStream_t s, EpiExtra ex = EpiExtra());
 void splitk_reduce(int M, int N, int splits, const float* part, float* C, int ldc, const float* relu_mask,
                    int ldm, cudaStream_t s);
 struct OutArgs {

@@ -406,10 +406,11 @@ int head_backward(mel_ctx* c) {
     nl += 1;
     if (l > 1) {
       const float* W = c->d_p + c->off[2 * (l - 1)];
-      nl += sgemm_auto(false, false, (int)c->B, din, dout, dZ, dout, W, din, c->d_dz[l - 2], din, EPI_STORE, nullptr,
-                       nullptr, 0, c->d_part, c->part_elems, c->stream);
-      relu_mask_mul(c->d_dz[l - 2], c->d_z[l - 2], (uint64_t)c->B * din, c->stream);
-      nl += 1;
+      EpiExtra ex;
+      ex.mask = c->d_z[l - 2];                   // dZ_{l-1} = dH_{l-1} * ReLU'(Z_{l-1}), fused
+      ex.ldm = din;
+      nl += sgemm_auto(false, false, (int)c->B, din, dout, dZ, dout, W, din, c->d_dz[l - 2], din, EPI_RELU_MASK,
+                       nullptr, nullptr, 0, c->d_part, c->part_elems, c->stream, ex);
     }
   }
   c->launches += nl;
@@ -417,15 +418,17 @@ int head_backward(mel_ctx* c) {
   return check_launch(c, "head backward");
 }
 
-int head_forward(mel_ctx* c, const float* xn, float** Z, float** H, int rows) {
+int head_forward(mel_ctx* c, const float* xn, float** Z, float** H, int rows, __nv_bfloat16* h_last_bf16 = nullptr) {
   int nl = 0;
   for (int l = 1; l < c->L; ++l) {
     const int din = c->dims[l - 1], dout = c->dims[l];
     const float* Hin = (l == 1) ? xn : H[l - 2];
     const int ldin = (l == 1) ? 8 : din;
+    EpiExtra ex;
+    if (l == c->L - 1) ex.Hb = h_last_bf16;     // bf16 operand of the tensor-core output layer
     nl += sgemm_auto(false, true, rows, dout, din, Hin, ldin, c->d_p + c->off[2 * (l - 1)], din, Z[l - 1], dout,
                      EPI_BIAS_RELU, c->d_p + c->off[2 * (l - 1) + 1], H[l - 1], dout, c->d_part, c->part_elems,
-                     c->stream);
+                     c->stream, ex);
   }
   return nl;
 }
@@ -472,10 +475,6 @@ int train_step_fp32(mel_ctx* c) {
 int train_step_bf16(mel_ctx* c) {
   const int L = c->L;
   const uint32_t B = c->B, K = c->Klast;
-  {
-    Timer t(c, MEL_K_HEAD_FWD, 1);
-    to_bf16(c->d_h[L - 2], c->tcb.h_bf16, (uint64_t)B * K, c->stream);
-  }
   tc::OutTcArgs a{};
   a.N = c->N; a.Npad = c->Npad; a.B = B; a.K = K;
   a.shadow_idx = c->shadow_cur;
@@ -1059,7 +1058,8 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
   }
   {
     Timer t(c, MEL_K_HEAD_FWD, 0);
-    const int nl = head_forward(c, c->d_xn, c->d_z, c->d_h, (int)c->B);
+    const int nl = head_forward(c, c->d_xn, c->d_z, c->d_h, (int)c->B,
+                                c->cfg.precision == MEL_BF16 ? c->tcb.h_bf16 : nullptr);
     c->launches += nl;
     c->klaunch[MEL_K_HEAD_FWD] += nl;
   }

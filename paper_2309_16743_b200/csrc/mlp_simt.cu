@@ -18,7 +18,7 @@ template <bool TA, bool TB>
 __global__ void __launch_bounds__(256)
 sgemm_kernel(int M, int N, int K, const float* __restrict__ A, int lda, const float* __restrict__ B, int ldb,
              float* __restrict__ C, int ldc, int epi, const float* __restrict__ bias, float* __restrict__ H, int ldh,
-             int k_chunk) {
+             int k_chunk, EpiExtra ex) {
   pdl_enter();
   __shared__ float As[TK][TM + 4];
   __shared__ float Bs[TK][TN + 4];
@@ -70,9 +70,14 @@ sgemm_kernel(int M, int N, int K, const float* __restrict__ A, int lda, const fl
       const int n = n0 + tx + 16 * j;
       if (n >= N) continue;
       float v = acc[i][j];
-      if (epi != EPI_STORE) v += bias[n];
+      if (epi == EPI_BIAS || epi == EPI_BIAS_RELU) v += bias[n];
+      if (epi == EPI_RELU_MASK && !(ex.mask[(size_t)m * ex.ldm + n] > 0.f)) v = 0.f;
       Cz[(size_t)m * ldc + n] = v;
-      if (epi == EPI_BIAS_RELU) H[(size_t)m * ldh + n] = fmaxf(v, 0.f);
+      if (epi == EPI_BIAS_RELU) {
+        const float h = fmaxf(v, 0.f);
+        H[(size_t)m * ldh + n] = h;
+        if (ex.Hb) ex.Hb[(size_t)m * ldh + n] = __float2bfloat16_rn(h);
+      }
     }
   }
 }
@@ -163,39 +168,53 @@ out_fwd_f32_kernel(OutArgs a) {
 
 // column sums over the batch: 32 columns x 8 row-groups per block, each thread a
 // fixed strided order, then the 8 partials in fixed order (deterministic)
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 col_sum_kernel(const float* __restrict__ X, int rows, int cols, int ld, float* __restrict__ out) {
   pdl_enter();
-  __shared__ float part[8][33];
+  // 32 columns x 32 row groups per CTA; each thread sums rows g, g+32, ... (4 loads in
+  // flight), then a fixed-order tree over the 32 groups: deterministic
+  __shared__ float part[32][33];
   const int cl = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + cl;
-  float s = 0.f;
-  if (c < cols)
-    for (int r = grp; r < rows; r += 8) s += X[(size_t)r * ld + c];
-  part[grp][cl] = s;
-  __syncthreads();
-  if (grp == 0 && c < cols) {
-    float t = 0.f;
-#pragma unroll
-    for (int g = 0; g < 8; ++g) t += part[g][cl];
-    out[c] = t;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  if (c < cols) {
+    int r = grp;
+    for (; r + 96 < rows; r += 128) {
+      s0 += X[(size_t)r * ld + c];
+      s1 += X[(size_t)(r + 32) * ld + c];
+      s2 += X[(size_t)(r + 64) * ld + c];
+      s3 += X[(size_t)(r + 96) * ld + c];
+    }
+    for (; r < rows; r += 32) s0 += X[(size_t)r * ld + c];
   }
+  part[grp][cl] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  for (int o = 16; o > 0; o >>= 1) {
+    if (grp < o) part[grp][cl] += part[grp + o][cl];
+    __syncthreads();
+  }
+  if (grp == 0 && c < cols) out[c] = part[0][cl];
 }
 
 // split-K reduction with the GEMM epilogues: out = sum_z part[z] (+ bias, then Z/H
 // with ReLU for EPI_BIAS_RELU), fixed order over z
 __global__ void splitk_reduce_epi_kernel(int M, int N, int splits, const float* __restrict__ part, float* __restrict__ C,
                                          int ldc, int epi, const float* __restrict__ bias, float* __restrict__ H,
-                                         int ldh) {
+                                         int ldh, EpiExtra ex) {
   pdl_enter();
   const size_t total = (size_t)M * N;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
     const int m = (int)(i / N), n = (int)(i % N);
     float v = 0.f;
     for (int z = 0; z < splits; ++z) v += part[(size_t)z * M * N + i];
-    if (epi != EPI_STORE) v += bias[n];
+    if (epi == EPI_BIAS || epi == EPI_BIAS_RELU) v += bias[n];
+    if (epi == EPI_RELU_MASK && !(ex.mask[(size_t)m * ex.ldm + n] > 0.f)) v = 0.f;
     C[(size_t)m * ldc + n] = v;
-    if (epi == EPI_BIAS_RELU) H[(size_t)m * ldh + n] = fmaxf(v, 0.f);
+    if (epi == EPI_BIAS_RELU) {
+      const float h = fmaxf(v, 0.f);
+      H[(size_t)m * ldh + n] = h;
+      if (ex.Hb) ex.Hb[(size_t)m * ldh + n] = __float2bfloat16_rn(h);
+    }
   }
 }
 
@@ -402,15 +421,15 @@ inline unsigned grid_for(uint64_t n, unsigned block = 256, unsigned cap = 148 * 
 }  // namespace
 
 void sgemm(bool ta, bool tb, int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
-           int ldc, int epi, const float* bias, float* H, int ldh, int splits, cudaStream_t s) {
+           int ldc, int epi, const float* bias, float* H, int ldh, int splits, cudaStream_t s, EpiExtra ex) {
   if (splits < 1) splits = 1;
   int k_chunk = (K + splits - 1) / splits;
   k_chunk = ((k_chunk + TK - 1) / TK) * TK;
   dim3 grid((N + TN - 1) / TN, (M + TM - 1) / TM, splits);
-  if (!ta && !tb) launch_pdl(sgemm_kernel<false, false>, dim3(grid), dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk);
-  else if (!ta && tb) launch_pdl(sgemm_kernel<false, true>, dim3(grid), dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk);
-  else if (ta && !tb) launch_pdl(sgemm_kernel<true, false>, dim3(grid), dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk);
-  else launch_pdl(sgemm_kernel<true, true>, dim3(grid), dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk);
+  if (!ta && !tb) launch_pdl(sgemm_kernel<false, false>, dim3(grid), dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk, ex);
+  else if (!ta && tb) launch_pdl(sgemm_kernel<false, true>, dim3(grid), dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk, ex);
+  else if (ta && !tb) launch_pdl(sgemm_kernel<true, false>, dim3(grid), dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk, ex);
+  else launch_pdl(sgemm_kernel<true, true>, dim3(grid), dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk, ex);
 }
 
 void splitk_reduce(int M, int N, int splits, const float* part, float* C, int ldc, const float* relu_mask, int ldm,
@@ -425,22 +444,23 @@ int out_fwd_f32(const OutArgs& a, cudaStream_t s) {
 }
 
 void col_sum(const float* X, int rows, int cols, int ld, float* out, cudaStream_t s) {
-  launch_pdl(col_sum_kernel, dim3((cols + 31) / 32), dim3(256), 0, s, X, rows, cols, ld, out);
+  launch_pdl(col_sum_kernel, dim3((cols + 31) / 32), dim3(1024), 0, s, X, rows, cols, ld, out);
 }
 
 // SIMT GEMM that fills the GPU: split-K through `scratch` (>= splits*M*N floats) when
 // the output grid is smaller than one wave; returns the number of launches
 int sgemm_auto(bool ta, bool tb, int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
-               int epi, const float* bias, float* H, int ldh, float* scratch, size_t scratch_elems, cudaStream_t s) {
+               int epi, const float* bias, float* H, int ldh, float* scratch, size_t scratch_elems, cudaStream_t s,
+               EpiExtra ex) {
   const int tiles = ((M + TM - 1) / TM) * ((N + TN - 1) / TN);
   int sk = 1;
   while (tiles * sk < 148 && K / (sk * 2) >= 64 && (size_t)(sk * 2) * M * N <= scratch_elems) sk *= 2;
   if (sk == 1) {
-    sgemm(ta, tb, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, 1, s);
+    sgemm(ta, tb, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, 1, s, ex);
     return 1;
   }
   sgemm(ta, tb, M, N, K, A, lda, B, ldb, scratch, N, EPI_STORE, nullptr, nullptr, 0, sk, s);
-  launch_pdl(splitk_reduce_epi_kernel, dim3(grid_for((uint64_t)M * N)), dim3(256), 0, s, M, N, sk, scratch, C, ldc, epi, bias, H, ldh);
+  launch_pdl(splitk_reduce_epi_kernel, dim3(grid_for((uint64_t)M * N)), dim3(256), 0, s, M, N, sk, scratch, C, ldc, epi, bias, H, ldh, ex);
   return 2;
 }
 
