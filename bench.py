@@ -427,14 +427,20 @@ def main():
                          "memory, surrogate_step_result) while the next step runs",
                "last_loss": losses[-1]}
 
-    # ---- validation MSE on one held-out simulation ----
+    # ---- validation MSE on 10 held-out simulations (the validation design stream) ----
     val = None
     try:
-        Xv = torch.from_numpy(design.draw_design(1, seed=1, validation=True)).to(dev)
+        n_val = 10
+        Xv = torch.from_numpy(design.draw_design(n_val, seed=1, validation=True)).to(dev)
         tv = torch.arange(TAU, device=dev)
-        Fv = heat_torch.fields(phi, Xv.repeat(TAU, 1), tv).cpu().numpy()
-        mse, _ = ctx.eval(Xv.repeat(TAU, 1).cpu().numpy(), tv.cpu().numpy().astype(np.uint32), Fv)
-        val = {"mse_normalised": mse, "mse_K2": mse * 400.0 ** 2, "samples": TAU}
+        sse, cnt = 0.0, 0
+        for i in range(n_val):                       # one simulation (100 time steps, 400 MB) at a time
+            Fv = heat_torch.fields(phi, Xv[i:i + 1].repeat(TAU, 1), tv).cpu().numpy()
+            mse, _ = ctx.eval(Xv[i:i + 1].repeat(TAU, 1).cpu().numpy(), tv.cpu().numpy().astype(np.uint32), Fv)
+            sse += mse * TAU
+            cnt += TAU
+        mse = sse / cnt
+        val = {"mse_normalised": mse, "mse_K2": mse * 400.0 ** 2, "samples": cnt, "simulations": n_val}
     except Exception as e:
         val = {"error": str(e)}
     stats = ctx.stats()
