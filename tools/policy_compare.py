@@ -3,8 +3,9 @@ shape (1000x1000 field, 6-256-256-10^6 MLP, B = 1024, C = 6000, theta = 1000):
 a wall-clock producer streams fields at a fixed rate with a production gap in the
 middle, the consumer loop samples and trains whenever its buffer gives a batch.
 Reported per policy: training throughput (samples consumed / s), steps, GPU time
-fraction spent training, unique samples ingested, repeats per unique sample, and
-the population at the end.  Usage:
+fraction spent training, unique samples ingested, repeats per unique sample, the
+population at the end, and the validation MSE on the 10 held-out simulations
+ after the same wall-clock budget (the paper's Table 1 comparison).  Usage:
     python tools/policy_compare.py [--rate 2000] [--seconds 6] [--gap 2,4]
 """
 import argparse
@@ -74,11 +75,22 @@ def run(policy, args):
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     st = ctx.stats()
+    # validation MSE on the 10 held-out simulations, after the same wall-clock budget
+    import numpy as np
+    Xv = torch.from_numpy(design.draw_design(10, seed=1, validation=True)).to(dev)
+    tv = torch.arange(tau, device=dev)
+    sse = 0.0
+    for i in range(10):
+        Fv = heat_torch.fields(phi, Xv[i:i + 1].repeat(tau, 1), tv).cpu().numpy()
+        mse, _ = ctx.eval(Xv[i:i + 1].repeat(tau, 1).cpu().numpy(), tv.cpu().numpy().astype(np.uint32), Fv)
+        sse += mse
+    val_mse = sse / 10
     uniq = st["committed"]
     name = {0: "reservoir", 1: "fifo", 2: "firo"}[policy]
     return {"policy": name, "steps": steps, "samples_per_s": steps * 1024 / wall, "gpu_busy_frac": busy / wall,
             "produced": sent, "unique_ingested": int(uniq), "repeats_per_unique": st["draws"] / max(1, uniq),
-            "population_end": int(st["population"]), "pending_end": int(st["pending"]), "wall_s": wall}
+            "population_end": int(st["population"]), "pending_end": int(st["pending"]), "wall_s": wall,
+            "val_mse_normalised": val_mse, "val_mse_K2": val_mse * 400.0 ** 2}
 
 
 def main():
@@ -92,12 +104,12 @@ def main():
     rows = [run(p, args) for p in (0, 1, 2)]
     for r in rows:
         print(json.dumps(r), flush=True)
-    print("\n| policy | steps | training samples/s | GPU busy | unique ingested | repeats / unique | population at end |")
-    print("|---|---|---|---|---|---|---|")
+    print("\n| policy | steps | training samples/s | GPU busy | unique ingested | repeats / unique | population at end | val MSE (K²) |")
+    print("|---|---|---|---|---|---|---|---|")
     for r in rows:
-        print("| %s | %d | %.0f | %.1f%% | %d | %.1f | %d |" % (r["policy"], r["steps"], r["samples_per_s"],
-                                                          100 * r["gpu_busy_frac"], r["unique_ingested"],
-                                                          r["repeats_per_unique"], r["population_end"]))
+        print("| %s | %d | %.0f | %.1f%% | %d | %.1f | %d | %.1f |" % (
+            r["policy"], r["steps"], r["samples_per_s"], 100 * r["gpu_busy_frac"], r["unique_ingested"],
+            r["repeats_per_unique"], r["population_end"], r["val_mse_K2"]))
 
 
 if __name__ == "__main__":
