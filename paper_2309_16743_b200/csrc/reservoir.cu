@@ -87,90 +87,88 @@ commit_ctrl(ResArgs a, uint64_t tail, uint32_t closed) {
     commit_queue(a, tail, closed);
     return;
   }
-  extern __shared__ uint32_t s_bits[];          // seen bitmap, ceil(C/32) words
-  __shared__ uint32_t s_warp[32];
-  __shared__ uint32_t s_cmd[4];                  // 0: mode (0 stop, 1 fill, 2 evict), 1: count / r, 2: result slot
+  // Seen bitmap + exclusive prefix of its word popcounts in SMEM.  One warp plans the
+  // puts in order (fill slots p, p+1, ...; full phase: evict the r-th seen slot, found by
+  // a binary search over the prefix and a find-n-th-set-bit, then the prefix updated
+  // lane-parallel); the whole block then applies the plan in parallel (metadata copy from
+  // the mapped staging entries, seen / put_seq reset, retired-count histogram).
+  extern __shared__ uint32_t s_dyn[];
   const uint32_t W = (a.C + 31) / 32;
+  uint32_t* s_bits = s_dyn;                      // [W]
+  uint32_t* s_pref = s_dyn + W;                  // [W + 1]
+  __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_res[3];                  // p, u, n_plan after planning (thread 0 -> block)
+  __shared__ uint32_t s_nev;
   for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) s_bits[i] = a.bitmap[i];
   ResDev* st = a.st;
   uint32_t p = st->p, u = st->u;
-  uint64_t q = st->q, consumed = st->consumed;
-  uint32_t n_plan = 0;
+  const uint64_t q0 = st->q, c0 = st->consumed;
   __syncthreads();
-  const uint32_t wpt = (W + blockDim.x - 1) / blockDim.x;   // words per thread
-  while (true) {
-    if (threadIdx.x == 0) {
-      if (consumed >= tail || u == a.C) {
-        s_cmd[0] = 0;                                        // P:264 "wait"
-      } else if (p < a.C) {
-        uint64_t avail = tail - consumed;
-        const uint64_t room = (uint64_t)(a.C - p);
-        const uint32_t cnt = (uint32_t)(avail < room ? avail : room);
-        s_cmd[0] = 1; s_cmd[1] = cnt;
-      } else {
-        uint32_t s = p - u;                                  // seen population
-        s_cmd[0] = 2;
-        s_cmd[1] = bounded(philox_r64(a.seed, TAG_EVICT, q, a.rank), s);
-      }
-    }
-    __syncthreads();
-    const uint32_t mode = s_cmd[0];
-    if (mode == 0) break;
-    if (mode == 1) {
-      // fill phase: dense prefix, slot = p + i (deterministic lane prefix)
-      const uint32_t cnt = s_cmd[1];
-      for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
-        const uint32_t j = p + i;
-        const uint32_t e = (uint32_t)((consumed + i) % a.S);
-        a.meta[j] = a.st_meta[e];
-        a.seen[j] = 0;
-        a.put_seq[j] = q + i;
-        a.plan[n_plan + i] = make_uint2(e, j);
-      }
-      p += cnt; u += cnt; q += cnt; consumed += cnt; n_plan += cnt;
-      __syncthreads();
-      continue;
-    }
-    // full phase: find the r-th set bit (ascending slot id) of the seen bitmap
-    const uint32_t r = s_cmd[1];
-    uint32_t cnt = 0;
+  {
+    const uint32_t wpt = (W + blockDim.x - 1) / blockDim.x;   // words per thread
     const uint32_t w0 = threadIdx.x * wpt;
+    uint32_t cnt = 0;
     for (uint32_t k = 0; k < wpt; ++k)
       if (w0 + k < W) cnt += __popc(s_bits[w0 + k]);
-    const uint32_t before = block_excl_scan(cnt, s_warp);
-    if (r >= before && r < before + cnt) {
-      uint32_t rem = r - before;
-      for (uint32_t k = 0; k < wpt; ++k) {
-        uint32_t word = s_bits[w0 + k];
-        uint32_t pc = __popc(word);
-        if (rem < pc) {
-          for (uint32_t b = 0; b < 32; ++b) {
-            if (word & (1u << b)) {
-              if (rem == 0) { s_cmd[2] = (w0 + k) * 32 + b; break; }
-              --rem;
-            }
-          }
-          break;
-        }
-        rem -= pc;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const uint32_t j = s_cmd[2];
-      const uint32_t e = (uint32_t)(consumed % a.S);
-      const uint32_t sc = a.seen[j];
-      st->hist[sc < HIST_BINS ? sc : HIST_BINS - 1] += 1;     // retired with its count
-      st->evictions += 1;
-      s_bits[j >> 5] &= ~(1u << (j & 31));
-      a.meta[j] = a.st_meta[e];
-      a.seen[j] = 0;
-      a.put_seq[j] = q;
-      a.plan[n_plan] = make_uint2(e, j);
-    }
-    q += 1; u += 1; consumed += 1; n_plan += 1;
-    __syncthreads();
+    uint32_t run = block_excl_scan(cnt, s_warp);
+    for (uint32_t k = 0; k < wpt; ++k)
+      if (w0 + k < W) { s_pref[w0 + k] = run; run += __popc(s_bits[w0 + k]); }
+    if (w0 < W && w0 + wpt >= W) s_pref[W] = run;
   }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const uint32_t lane = threadIdx.x;
+    uint64_t consumed = c0;
+    uint32_t n_plan = 0, n_ev = 0;
+    while (consumed < tail && u < a.C) {                      // all unseen -> wait
+      if (p < a.C) {                                          // fill phase: dense prefix
+        const uint64_t avail = tail - consumed, room = (uint64_t)(a.C - p);
+        const uint32_t cnt = (uint32_t)(avail < room ? avail : room);
+        for (uint32_t i = lane; i < cnt; i += 32)
+          a.plan[n_plan + i] = make_uint2((uint32_t)((consumed + i) % a.S), p + i);
+        p += cnt; u += cnt; consumed += cnt; n_plan += cnt;
+        continue;
+      }
+      // full phase: the r-th seen slot in ascending slot id, r ~ Philox EVICT(q)
+      uint32_t w = 0, j = 0;
+      if (lane == 0) {
+        const uint32_t r = bounded(philox_r64(a.seed, TAG_EVICT, q0 + n_plan, a.rank), p - u);
+        uint32_t lo = 0, hi = W;                              // largest w with pref[w] <= r
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (s_pref[mid] <= r) lo = mid; else hi = mid;
+        }
+        w = lo;
+        j = w * 32 + __fns(s_bits[w], 0, (int)(r - s_pref[w]) + 1);
+        s_bits[w] &= ~(1u << (j & 31));                       // the new item is unseen
+      }
+      w = __shfl_sync(0xffffffffu, w, 0);
+      j = __shfl_sync(0xffffffffu, j, 0);
+      for (uint32_t i = w + 1 + lane; i <= W; i += 32) s_pref[i] -= 1;
+      if (lane == 0) a.plan[n_plan] = make_uint2((uint32_t)(consumed % a.S), j | 0x80000000u);
+      __syncwarp();
+      u += 1; consumed += 1; n_plan += 1; n_ev += 1;
+    }
+    if (lane == 0) { s_res[0] = p; s_res[1] = u; s_res[2] = n_plan; s_nev = n_ev; }
+  }
+  __syncthreads();
+  p = s_res[0]; u = s_res[1];
+  const uint32_t n_plan = s_res[2];
+  const uint64_t q = q0 + n_plan, consumed = c0 + n_plan;
+  for (uint32_t i = threadIdx.x; i < n_plan; i += blockDim.x) {
+    const uint2 ej = a.plan[i];
+    const uint32_t j = ej.y & 0x7FFFFFFFu;
+    if (ej.y & 0x80000000u) {                                 // evictee retired with its count
+      const uint32_t sc = a.seen[j];
+      atomicAdd(reinterpret_cast<unsigned long long*>(&st->hist[sc < HIST_BINS ? sc : HIST_BINS - 1]), 1ull);
+    }
+    a.meta[j] = a.st_meta[ej.x];
+    a.seen[j] = 0;
+    a.put_seq[j] = q0 + i;
+    a.plan[i] = make_uint2(ej.x, j);
+  }
+  if (threadIdx.x == 0) st->evictions += s_nev;
+  __syncthreads();
   for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) a.bitmap[i] = s_bits[i];
   if (threadIdx.x == 0) {
     st->p = p; st->u = u; st->q = q; st->consumed = consumed; st->n_plan = n_plan;
@@ -367,7 +365,7 @@ __global__ void init_res(ResArgs a) {
 
 void launch_commit(const ResArgs& a, uint64_t tail, uint32_t closed, uint32_t max_entries, cudaStream_t s) {
   const uint32_t W = (a.C + 31) / 32;
-  const size_t smem = (size_t)W * 4;
+  const size_t smem = (size_t)(2 * W + 1) * 4;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(commit_ctrl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   launch_pdl(commit_ctrl, dim3(1), dim3(CTRL_THREADS), smem, s, a, tail, closed);
