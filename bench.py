@@ -460,7 +460,10 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "val_mse": val,
             "reservoir": {"population": stats["population"], "unseen": stats["unseen"],
                           "evictions": stats["evictions"], "puts": stats["puts"], "draws": stats["draws"],
-                          "repeats_per_unique": stats["draws"] / max(1, stats["committed"])}}
+                          "repeats_per_unique": stats["draws"] / max(1, stats["committed"]),
+                          # how many times the evicted items had been seen (retired-count
+                          # histogram, last bin saturates), as {seen_count: items}
+                          "evicted_seen_hist": {int(i): int(v) for i, v in enumerate(stats["hist"]) if v}}}
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close_ctx()
