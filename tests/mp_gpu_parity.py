@@ -34,12 +34,14 @@ def main():
     # bf16: in-kernel NVLink exchange (default); bf16-nccl: NCCL reduce-scatter / all-gather
     flags = (mel.FLAG_NCCL_EXCHANGE if mode.endswith("-nccl") else
              mel.FLAG_FP32_EXCHANGE if mode.endswith("-fp32x") else 0)
+    # fp32-fifo / fp32-firo: the comparison buffers on every rank
+    policy = ores.FIFO if mode.endswith("-fifo") else ores.FIRO if mode.endswith("-firo") else ores.RESERVOIR
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(rank)
     dist.init_process_group("gloo")
     obj = [mel.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    if mode == "fp32":
+    if mode.startswith("fp32"):
         wl = replace(design.TINY_EVICT, world=world, puts_per_step=10)
         prec = store = 0
         tol_loss, tol_w, max_steps = 1e-5, 1e-5, None
@@ -49,9 +51,10 @@ def main():
         prec = store = 1
         tol_loss, tol_w, max_steps = 2e-2, 1e-3, 5
     table = FieldTable(wl)
-    ctx = mel.Context(make_config(wl, precision=prec, storage=store, flags=flags), rank=rank, world=world, nccl_id=obj[0],
-                      device=rank)
-    res = [ores.Reservoir(wl.capacity, wl.threshold, wl.n_field, seed=1, rank=r, storage=store) for r in range(world)]
+    ctx = mel.Context(make_config(wl, precision=prec, storage=store, flags=flags, policy=policy), rank=rank, world=world,
+                      nccl_id=obj[0], device=rank)
+    res = [ores.Reservoir(wl.capacity, wl.threshold, wl.n_field, seed=1, rank=r, storage=store, policy=policy)
+           for r in range(world)]
     batches = [[] for _ in range(world)]
     steps, worst_l, worst_w = 0, 0.0, 0.0
     for op in design.build_oplog(wl):

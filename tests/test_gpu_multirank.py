@@ -16,12 +16,13 @@ def _ngpu():
 
 
 @pytest.mark.parametrize("world,mode", [(2, "fp32"), (2, "bf16"), (2, "bf16-nccl"), (2, "bf16-fp32x"), (4, "bf16"),
-                                        (4, "bf16-fp32x")])
+                                        (4, "bf16-fp32x"), (2, "fp32-fifo"), (2, "fp32-firo")])
 def test_multi_rank_parity(world, mode):
     """fp32: NCCL all-reduce; bf16: the in-kernel NVLink exchange (dW tiles reduce-added
     into their owner's buffer, fused Adam at the owner, shadow rows pushed to every rank);
     bf16-nccl: reduce-scatter / sharded Adam / all-gather through NCCL; bf16-fp32x: the
-    in-kernel exchange with fp32 contributions (default: bf16)."""
+    in-kernel exchange with fp32 contributions (default: bf16); fp32-fifo / fp32-firo: the
+    comparison buffers on every rank."""
     if _ngpu() < world:
         pytest.skip("needs %d GPUs" % world)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=%d" % world,
