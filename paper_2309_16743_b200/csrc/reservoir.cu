@@ -184,25 +184,28 @@ template <int STORAGE>
 __global__ void __launch_bounds__(256)
 commit_copy(ResArgs a) {
   pdl_enter();
-  const uint32_t y = blockIdx.y;
-  if (y >= a.st->n_plan) return;
-  const uint2 ej = a.plan[y];
-  const float4* src = reinterpret_cast<const float4*>(a.st_field + (uint64_t)ej.x * a.Npad);
+  // a fixed grid strides over every committed entry (the host only knows an upper bound
+  // on their number): 16-byte loads of the staged fp32 field, normalised on the fly
+  const uint32_t n_plan = a.st->n_plan;
   const uint32_t n4 = (a.N + 3) / 4;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
-    float4 v = __ldg(src + i);
-    float o[4] = {v.x, v.y, v.z, v.w};
+  for (uint32_t y = 0; y < n_plan; ++y) {
+    const uint2 ej = a.plan[y];
+    const float4* src = reinterpret_cast<const float4*>(a.st_field + (uint64_t)ej.x * a.Npad);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+      float4 v = __ldg(src + i);
+      float o[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int c = 0; c < 4; ++c) o[c] = (4 * i + c < a.N) ? normalise_rn(o[c], a.lo, a.span) : 0.f;
-    if (STORAGE == 0) {
-      float4* dst = reinterpret_cast<float4*>(static_cast<float*>(a.payload) + (uint64_t)ej.y * a.Npad);
-      dst[i] = make_float4(o[0], o[1], o[2], o[3]);
-    } else {
-      __nv_bfloat162 lo = __floats2bfloat162_rn(o[0], o[1]);   // RNE
-      __nv_bfloat162 hi = __floats2bfloat162_rn(o[2], o[3]);
-      uint2 pk = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
-      uint2* dst = reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.payload) + (uint64_t)ej.y * a.Npad);
-      dst[i] = pk;
+      for (int c = 0; c < 4; ++c) o[c] = (4 * i + c < a.N) ? normalise_rn(o[c], a.lo, a.span) : 0.f;
+      if (STORAGE == 0) {
+        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(a.payload) + (uint64_t)ej.y * a.Npad);
+        dst[i] = make_float4(o[0], o[1], o[2], o[3]);
+      } else {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(o[0], o[1]);   // RNE
+        __nv_bfloat162 hi = __floats2bfloat162_rn(o[2], o[3]);
+        uint2 pk = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+        uint2* dst = reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(a.payload) + (uint64_t)ej.y * a.Npad);
+        dst[i] = pk;
+      }
     }
   }
 }
@@ -372,8 +375,9 @@ void launch_commit(const ResArgs& a, uint64_t tail, uint32_t closed, uint32_t ma
   if (max_entries == 0) return;
   const uint32_t n4 = (a.N + 3) / 4;
   uint32_t gx = (n4 + 255) / 256;
-  if (gx > 512) gx = 512;
-  dim3 grid(gx, max_entries);
+  const uint32_t cap = 148u * 4u * (max_entries < 4 ? max_entries : 4u);   // ~ one wave per 4 entries
+  if (gx > cap) gx = cap;
+  dim3 grid(gx);
   if (a.storage == 0) launch_pdl(commit_copy<0>, dim3(grid), dim3(256), 0, s, a);
   else launch_pdl(commit_copy<1>, dim3(grid), dim3(256), 0, s, a);
 }
