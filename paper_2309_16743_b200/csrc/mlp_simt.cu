@@ -166,17 +166,18 @@ out_fwd_f32_kernel(OutArgs a) {
   if (threadIdx.x == 0) a.sse_part[blockIdx.y * gridDim.x + blockIdx.x] = s_red[0];
 }
 
-// column sums over the batch: 32 columns x 8 row-groups per block, each thread a
-// fixed strided order, then the 8 partials in fixed order (deterministic)
+// column sums over the batch (bias gradients): 32 columns x 32 row groups per CTA; each
+// thread sums rows g, g+32, ... (4 loads in flight), then a fixed-order tree over the 32
+// groups.  Accumulated in fp64 and rounded once, so the result is the fp32 rounding of the
+// (near-)exact sum whatever the order -- closest to the fp64 oracle and insensitive to the
+// grouping (the free-running bf16 trajectory amplifies fp32 order effects)
 __global__ void __launch_bounds__(1024)
 col_sum_kernel(const float* __restrict__ X, int rows, int cols, int ld, float* __restrict__ out) {
   pdl_enter();
-  // 32 columns x 32 row groups per CTA; each thread sums rows g, g+32, ... (4 loads in
-  // flight), then a fixed-order tree over the 32 groups: deterministic
-  __shared__ float part[32][33];
+  __shared__ double part[32][33];
   const int cl = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + cl;
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   if (c < cols) {
     int r = grp;
     for (; r + 96 < rows; r += 128) {
@@ -193,7 +194,7 @@ col_sum_kernel(const float* __restrict__ X, int rows, int cols, int ld, float* _
     if (grp < o) part[grp][cl] += part[grp + o][cl];
     __syncthreads();
   }
-  if (grp == 0 && c < cols) out[c] = part[0][cl];
+  if (grp == 0 && c < cols) out[c] = (float)part[0][cl];
 }
 
 // split-K reduction with the GEMM epilogues: out = sum_z part[z] (+ bias, then Z/H

@@ -29,3 +29,4 @@ for seed in [int(x) for x in sys.argv[1:]]:
     e = (np.array(lg) - np.array(lo)) / np.array(lo)
     print("seed %d: signed rel err step1000 %+.2e | mean|e| 951-1000 %.2e | mean signed 951-1000 %+.2e | loss %.3e" %
           (seed, e[-1], np.abs(e[-50:]).mean(), e[-50:].mean(), lo[-1]), flush=True)
+    print("   rel err at steps 100..1000:", " ".join("%+.1e" % e[i - 1] for i in range(100, 1001, 100)), flush=True)
