@@ -194,6 +194,23 @@ int mel_set_state(mel_ctx* ctx, const mel_state_view* in);
 int reservoir_put(mel_ctx* ctx, uint32_t sim_id, uint32_t t, const float X_host[5],
                   const float* field, int field_on_device);
 
+/* Drains up to max_msgs first-copy time steps from an ingest ring (include/mel_ingest.h,
+ * SURVEY §8(f) f2) into the buffer: each is a reservoir_put of the message's (sim_id, t,
+ * X, field), the field DMA-copied straight from the shared segment (page-locked on first
+ * use), in the ring's arrival order; a call's slots are released to the clients once
+ * its copies have landed (checked at the next call, at most 7 calls in flight; the
+ * ring must not be consumed elsewhere meanwhile, and must outlive the context or its
+ * last reservoir_ingest).  Waits up to timeout_us for the first message only.  Stops early
+ * when the staging ring is full (sample to reach a commit point) or nothing is published.
+ * *n_put_host = messages put.  MEL_EOS when the ring reports every expected client
+ * finalized and drained and nothing was put; MEL_ECLOSED after reservoir_close. */
+#ifndef MEL_INGEST_TYPEDEF_
+#define MEL_INGEST_TYPEDEF_
+typedef struct mel_ingest mel_ingest;
+#endif
+int reservoir_ingest(mel_ctx* ctx, mel_ingest* ing, uint32_t max_msgs, uint32_t timeout_us,
+                     uint32_t* n_put_host);
+
 /* Signals that reception is over ("When all the simulation data have been
  * generated the blocking related to the threshold is lifted").  Commits pending
  * puts.  A second call returns MEL_EPROTO. */

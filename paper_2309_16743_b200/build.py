@@ -16,7 +16,8 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 OUT = os.path.join(HERE, "libmel.so")
 OBJ = os.path.join(HERE, "build_obj")
-SOURCES = ["mel.cu", "reservoir.cu", "mlp_simt.cu", "tc_out.cu"]
+SOURCES = ["mel.cu", "reservoir.cu", "mlp_simt.cu", "tc_out.cu", "ingest.cpp"]
+INGEST_OUT = os.path.join(HERE, "libmel_ingest.so")   # host-only, for the simulation clients
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -31,7 +32,8 @@ def nccl_dirs():
 
 
 def _deps_mtime():
-    files = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "mel.h")]
+    files = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", f)
+                                                                  for f in ("mel.h", "mel_ingest.h")]
     return max(os.path.getmtime(f) for f in files)
 
 
@@ -39,13 +41,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     inc, lib = nccl_dirs()
     os.makedirs(OBJ, exist_ok=True)
     dep_t = _deps_mtime()
-    if not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= dep_t:
+    if (not force and os.path.exists(OUT) and os.path.getmtime(OUT) >= dep_t and os.path.exists(INGEST_OUT)
+            and os.path.getmtime(INGEST_OUT) >= dep_t):
         return OUT
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", inc,
                     "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
     def compile_one(src):
-        obj = os.path.join(OBJ, src.replace(".cu", ".o"))
+        obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
         cmd = [NVCC, "-c", os.path.join(CSRC, src), "-o", obj] + flags
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -63,6 +66,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError("link failed:\n%s\n%s" % (r.stdout, r.stderr))
     os.replace(tmp, OUT)
+    # the clients' library: the same ingest source, host compiler only, no CUDA dependency
+    tmp = INGEST_OUT + ".tmp"
+    cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"),
+           os.path.join(CSRC, "ingest.cpp"), "-o", tmp]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("ingest library build failed:\n%s\n%s" % (r.stdout, r.stderr))
+    os.replace(tmp, INGEST_OUT)
     return OUT
 
 

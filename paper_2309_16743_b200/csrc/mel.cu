@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../../include/mel.h"
+#include "../../include/mel_ingest.h"
 #include "kernels.h"
 #include "tc_out.h"
 
@@ -60,6 +61,14 @@ struct mel_ctx {
   bool closed = false;
   bool copy_pending = false;
   cudaEvent_t ev_copy = nullptr, ev_fence = nullptr;
+  void* ing_base = nullptr;                 // ingest segment page-locked for DMA (reservoir_ingest)
+  uint64_t ing_bytes = 0;
+  bool ing_pinned = false;
+  static constexpr int ING_EVENTS = 8;      // deferred slot releases: one event per ingest call
+  cudaEvent_t ing_ev[ING_EVENTS] = {};
+  uint32_t ing_cnt[ING_EVENTS] = {};
+  uint32_t ing_head = 0, ing_n = 0;         // FIFO of (event, message count) not yet released
+  mel_ingest* ing_handle = nullptr;
   int32_t* d_slots = nullptr;
   bool batch_known = false;        // host knows the last batch size
   uint32_t batch_n = 0;
@@ -831,6 +840,10 @@ void mel_destroy(mel_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->dev);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+  for (auto& e : c->ing_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->ing_pinned) cudaHostUnregister(c->ing_base);
   if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
   if (c->peer) {
     for (int q = 0; q < c->world; ++q) {
@@ -993,6 +1006,87 @@ int reservoir_put(mel_ctx* c, uint32_t sim, uint32_t t, const float X[5], const 
   }
   c->tail += 1;
   return MEL_OK;
+}
+
+// releases the slots of ingest calls whose DMA has landed; with `block`, waits for the
+// oldest one first
+int ingest_retire(mel_ctx* c, bool block) {
+  while (c->ing_n) {
+    const uint32_t i = c->ing_head;
+    if (block) {
+      CK(cudaEventSynchronize(c->ing_ev[i]));
+      block = false;
+    } else {
+      const cudaError_t q = cudaEventQuery(c->ing_ev[i]);
+      if (q == cudaErrorNotReady) break;
+      if (q != cudaSuccess) return fail(c, MEL_ECUDA, "ingest copy: %s", cudaGetErrorString(q));
+    }
+    for (uint32_t k = 0; k < c->ing_cnt[i]; ++k) mel_ingest_release(c->ing_handle);
+    c->ing_head = (i + 1) % mel_ctx::ING_EVENTS;
+    c->ing_n -= 1;
+  }
+  return MEL_OK;
+}
+
+int reservoir_ingest(mel_ctx* c, mel_ingest* g, uint32_t max_msgs, uint32_t timeout_us, uint32_t* n_put_host) {
+  GUARD(c);
+  if (!g) return fail(c, MEL_EINVAL, "null ingest handle");
+  if (n_put_host) *n_put_host = 0;
+  if (c->closed) return fail(c, MEL_ECLOSED, "reservoir_ingest after reservoir_close");
+  if (g != c->ing_handle) {
+    int r = ingest_retire(c, true);
+    while (!r && c->ing_n) r = ingest_retire(c, true);
+    if (r) return r;
+    c->ing_handle = g;
+  }
+  void* base = nullptr;
+  uint64_t bytes = 0;
+  mel_ingest_segment(g, &base, &bytes);
+  if (base != c->ing_base) {
+    // page-lock the shared segment once, so each field is DMA-copied straight from the
+    // client's slot into the staging ring (no bounce through pageable memory)
+    if (c->ing_pinned) CK(cudaHostUnregister(c->ing_base));
+    c->ing_base = base;
+    c->ing_bytes = bytes;
+    c->ing_pinned = cudaHostRegister(base, bytes, cudaHostRegisterDefault) == cudaSuccess;
+    if (!c->ing_pinned) (void)cudaGetLastError();   // pageable copies still work, synchronously
+  }
+  if (!c->ing_ev[0])
+    for (auto& e : c->ing_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // slots whose copies have landed go back to the clients; keep at most ING_EVENTS - 1
+  // calls in flight
+  int r = ingest_retire(c, c->ing_n == mel_ctx::ING_EVENTS);
+  if (r) return r;
+  uint32_t n = 0;
+  bool eos = false;
+  while (n < max_msgs) {
+    r = ensure_ring_space(c);
+    if (r == MEL_EAGAIN) break;                     // staging full: the caller samples (commit point)
+    if (r) return r;
+    mel_ingest_msg m;
+    int q = mel_ingest_next(g, &m, 0u);
+    if (q == MEL_EAGAIN && c->ing_n) {              // the ring may be waiting for our releases
+      if ((r = ingest_retire(c, true))) return r;
+      q = mel_ingest_next(g, &m, 0u);
+    }
+    if (q == MEL_EAGAIN && n == 0 && timeout_us) q = mel_ingest_next(g, &m, timeout_us);
+    if (q == MEL_EAGAIN) break;
+    if (q == MEL_EOS) { eos = true; break; }
+    if (q != MEL_OK) return fail(c, q, "ingest ring: status %d", q);
+    r = reservoir_put(c, m.sim_id, m.t, m.X, m.field, 0);
+    if (r) return r;
+    ++n;
+  }
+  if (n) {
+    // the slots go back to the clients once this call's copies have landed
+    const uint32_t i = (c->ing_head + c->ing_n) % mel_ctx::ING_EVENTS;
+    CK(cudaEventRecord(c->ing_ev[i], c->copy_stream));
+    c->ing_cnt[i] = n;
+    c->ing_n += 1;
+    if (!c->ing_pinned && (r = ingest_retire(c, true))) return r;
+  }
+  if (n_put_host) *n_put_host = n;
+  return (eos && n == 0) ? MEL_EOS : MEL_OK;
 }
 
 int reservoir_close(mel_ctx* c) {

@@ -36,7 +36,12 @@ EXPORTS = ["mel_config_default", "mel_nccl_unique_id", "mel_create", "mel_destro
            "reservoir_put", "reservoir_close", "reservoir_sample_batch", "surrogate_step", "surrogate_step_result",
            "surrogate_eval",
            "reservoir_stats", "reservoir_dump", "mel_sync", "mel_kernel_time", "mel_kernel_time_reset",
-           "mel_launch_count", "mel_set_flags", "mel_debug_counters"]
+           "mel_launch_count", "mel_set_flags", "mel_debug_counters", "reservoir_ingest"]
+# include/mel_ingest.h (host-only ingest channel; in libmel.so and libmel_ingest.so)
+INGEST_EXPORTS = ["mel_ingest_create", "mel_ingest_next", "mel_ingest_release", "mel_ingest_outstanding",
+                  "mel_ingest_stats_get", "mel_ingest_segment", "mel_ingest_destroy", "mel_client_open",
+                  "mel_client_send", "mel_client_finalize", "mel_client_close", "mel_route"]
+INGEST_LIB_PATH = os.path.join(HERE, "libmel_ingest.so")
 
 
 class MelError(RuntimeError):
@@ -67,7 +72,56 @@ class _StateView(C.Structure):
                 ("adam_step", C.c_uint64), ("samples_seen", C.c_uint64)]
 
 
+class _IngestMsg(C.Structure):
+    _fields_ = [("sim_id", C.c_uint32), ("t", C.c_uint32), ("X", C.c_float * 5), ("pad", C.c_uint32),
+                ("field", C.POINTER(C.c_float)), ("ticket", C.c_uint64)]
+
+
+class _IngestStats(C.Structure):
+    _fields_ = [("received", C.c_uint64), ("duplicates", C.c_uint64), ("abandoned", C.c_uint64),
+                ("finalized", C.c_uint64), ("clients", C.c_uint64), ("bytes", C.c_uint64)]
+
+
+def _ingest_sigs():
+    vp, u32, u64 = C.c_void_p, C.c_uint32, C.c_uint64
+    return {
+        "mel_ingest_create": (C.c_int, [C.c_char_p, u32, u32, u32, u32, C.POINTER(vp)]),
+        "mel_ingest_next": (C.c_int, [vp, C.POINTER(_IngestMsg), u32]),
+        "mel_ingest_release": (C.c_int, [vp]),
+        "mel_ingest_outstanding": (u32, [vp]),
+        "mel_ingest_stats_get": (C.c_int, [vp, C.POINTER(_IngestStats)]),
+        "mel_ingest_segment": (C.c_int, [vp, C.POINTER(vp), C.POINTER(u64)]),
+        "mel_ingest_destroy": (None, [vp]),
+        "mel_client_open": (C.c_int, [C.c_char_p, u32, u32, C.POINTER(vp)]),
+        "mel_client_send": (C.c_int, [vp, u32, C.POINTER(C.c_float), C.POINTER(C.c_double), u32]),
+        "mel_client_finalize": (C.c_int, [vp, u32]),
+        "mel_client_close": (None, [vp]),
+        "mel_route": (u32, [u32, u32, u32]),
+    }
+
+
+def _bind(lib, sig):
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+
+
 _lib = None
+_ingest_lib = None
+
+
+def load_ingest_library(path: str = INGEST_LIB_PATH):
+    """libmel_ingest.so: the clients' side of the ingest channel (host code only, no CUDA)."""
+    global _ingest_lib
+    if _ingest_lib is not None:
+        return _ingest_lib
+    if not os.path.exists(path):
+        raise OSError("libmel_ingest.so not built at %s (run python -m paper_2309_16743_b200.build)" % path)
+    lib = C.CDLL(path)
+    _bind(lib, _ingest_sigs())
+    _ingest_lib = lib
+    return lib
 
 
 def load_library(path: str = LIB_PATH):
@@ -105,11 +159,10 @@ def load_library(path: str = LIB_PATH):
         "mel_launch_count": (C.c_int, [vp, C.POINTER(u64)]),
         "mel_set_flags": (C.c_int, [vp, u32]),
         "mel_debug_counters": (C.c_int, [vp, C.POINTER(u64), C.c_int]),
+        "reservoir_ingest": (C.c_int, [vp, vp, u32, u32, C.POINTER(u32)]),
     }
-    for name, (res, args) in sig.items():
-        fn = getattr(lib, name)
-        fn.restype = res
-        fn.argtypes = args
+    sig.update(_ingest_sigs())
+    _bind(lib, sig)
     _lib = lib
     return lib
 
@@ -217,6 +270,13 @@ class Context:
 
     def close(self) -> int:
         return self._check(self.lib.reservoir_close(self.h))
+
+    def ingest(self, ing: "Ingest", max_msgs: int = 1 << 30, timeout_us: int = 0):
+        """reservoir_ingest: put up to max_msgs first-copy messages of an ingest ring.
+        Returns (status, n_put); status OK or EOS."""
+        n = C.c_uint32(0)
+        st = self._check(self.lib.reservoir_ingest(self.h, ing.h, max_msgs, timeout_us, C.byref(n)), (OK, EOS))
+        return st, n.value
 
     def sample(self, want_slots: bool = False, want_n: bool = False):
         """Returns (status, slots or None, n or None)."""
@@ -332,3 +392,81 @@ class Context:
         n = C.c_uint64()
         self._check(self.lib.mel_launch_count(self.h, C.byref(n)))
         return n.value
+
+
+class Ingest:
+    """Server side of one rank's ingest ring (include/mel_ingest.h)."""
+
+    def __init__(self, name: str, rank: int, n_field: int, slots: int, expected_clients: int = 0, lib=None):
+        self.lib = lib or load_library()
+        self.h = C.c_void_p()
+        st = self.lib.mel_ingest_create(name.encode(), rank, n_field, slots, expected_clients, C.byref(self.h))
+        if st != OK:
+            raise MelError(st, "mel_ingest_create(%s, %d)" % (name, rank))
+        self.n_field = n_field
+
+    def next(self, timeout_us: int = 0):
+        """(status, msg) with msg = dict(sim_id, t, X, field (a copy), ticket) when status == OK."""
+        m = _IngestMsg()
+        st = self.lib.mel_ingest_next(self.h, C.byref(m), timeout_us)
+        if st < 0:
+            raise MelError(st, "mel_ingest_next")
+        if st != OK:
+            return st, None
+        field = np.ctypeslib.as_array(m.field, shape=(self.n_field,)).copy()
+        return st, dict(sim_id=m.sim_id, t=m.t, X=np.array(m.X[:], dtype=np.float32), field=field, ticket=m.ticket)
+
+    def release(self):
+        st = self.lib.mel_ingest_release(self.h)
+        if st != OK:
+            raise MelError(st, "mel_ingest_release")
+
+    def outstanding(self) -> int:
+        return int(self.lib.mel_ingest_outstanding(self.h))
+
+    def stats(self) -> dict:
+        s = _IngestStats()
+        self.lib.mel_ingest_stats_get(self.h, C.byref(s))
+        return {k: int(getattr(s, k)) for k, _ in _IngestStats._fields_}
+
+    def destroy(self):
+        if self.h:
+            self.lib.mel_ingest_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+class Client:
+    """A simulation client: init_communication / send / finalize_communication."""
+
+    def __init__(self, name: str, world: int, client_id: int, lib=None):
+        self.lib = lib or load_ingest_library()
+        self.h = C.c_void_p()
+        st = self.lib.mel_client_open(name.encode(), world, client_id, C.byref(self.h))
+        if st != OK:
+            raise MelError(st, "mel_client_open(%s)" % name)
+
+    def send(self, t: int, X, field_f64, timeout_us: int = 10_000_000) -> int:
+        Xa = np.ascontiguousarray(X, dtype=np.float32)
+        f = np.ascontiguousarray(field_f64, dtype=np.float64)
+        st = self.lib.mel_client_send(self.h, t, Xa.ctypes.data_as(C.POINTER(C.c_float)),
+                                      f.ctypes.data_as(C.POINTER(C.c_double)), timeout_us)
+        if st < 0:
+            raise MelError(st, "mel_client_send")
+        return st
+
+    def finalize(self, timeout_us: int = 10_000_000) -> int:
+        st = self.lib.mel_client_finalize(self.h, timeout_us)
+        if st < 0:
+            raise MelError(st, "mel_client_finalize")
+        return st
+
+    def close(self):
+        if self.h:
+            self.lib.mel_client_close(self.h)
+            self.h = C.c_void_p()

@@ -20,11 +20,33 @@ def lib():
     return mel.load_library()
 
 
-def declared_functions():
-    src = open(HEADER).read()
+def declared_functions(header=HEADER):
+    src = open(header).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    names = re.findall(r"^\s*(?:int|void|const char\*)\s+\**(\w+)\s*\(", src, flags=re.M)
+    names = re.findall(r"^\s*(?:int|void|uint32_t|const char\*)\s+\**(\w+)\s*\(", src, flags=re.M)
     return sorted(set(names))
+
+
+INGEST_HEADER = os.path.join(ROOT, "include", "mel_ingest.h")
+
+
+def _exported(so):
+    out = subprocess.run(["nm", "-D", "--defined-only", os.path.join(PKG, so)], capture_output=True, text=True).stdout
+    return set(l.split()[-1] for l in out.splitlines() if " T " in l)
+
+
+def test_ingest_header_exported_by_both_libraries(lib):
+    """include/mel_ingest.h: the server side lives in libmel.so, the clients load
+    libmel_ingest.so, which must not depend on CUDA (clients run on host cores)."""
+    from paper_2309_16743_b200 import mel
+    names = declared_functions(INGEST_HEADER)
+    assert sorted(mel.INGEST_EXPORTS) == names
+    for so in ("libmel.so", "libmel_ingest.so"):
+        missing = [n for n in names if n not in _exported(so)]
+        assert not missing, (so, missing)
+    deps = subprocess.run(["ldd", os.path.join(PKG, "libmel_ingest.so")], capture_output=True, text=True).stdout
+    assert "cuda" not in deps and "nccl" not in deps
+    mel.load_ingest_library()
 
 
 def test_header_declares_the_paper_calls():
