@@ -211,6 +211,23 @@ typedef struct mel_ingest mel_ingest;
 int reservoir_ingest(mel_ctx* ctx, mel_ingest* ing, uint32_t max_msgs, uint32_t timeout_us,
                      uint32_t* n_put_host);
 
+/* The offline baseline: trains on batches first_batch ..
+ * first_batch + n_batches - 1 of epoch `epoch` of a file dataset (include/mel_dataset.h;
+ * order = reading R24 with `seed`; the last partial batch of an epoch is dropped) on the
+ * same trainer: each record is a reservoir_put of its field (read by the dataset's loader
+ * threads into pinned chunk buffers, double-buffered against the DMA), and every B puts
+ * are handed out by the FIFO buffer as one batch (reservoir_sample_batch) and trained
+ * (surrogate_step).  Requires mel_config.policy = MEL_FIFO and staging_entries >= batch.
+ * losses_host (NULL or >= n_batches doubles) receives each step's loss;
+ * *steps_host = steps done. */
+#ifndef MEL_DATASET_TYPEDEF_
+#define MEL_DATASET_TYPEDEF_
+typedef struct mel_dataset mel_dataset;
+#endif
+int surrogate_train_offline(mel_ctx* ctx, mel_dataset* ds, uint64_t seed, uint32_t epoch,
+                            uint32_t first_batch, uint32_t n_batches, double* losses_host,
+                            uint32_t* steps_host);
+
 /* Signals that reception is over ("When all the simulation data have been
  * generated the blocking related to the threshold is lifted").  Commits pending
  * puts.  A second call returns MEL_EPROTO. */

@@ -32,6 +32,7 @@ TAG_SAMPLE = 1
 TAG_EVICT = 2
 TAG_DRAIN = 3
 TAG_INIT = 4
+TAG_EPOCH = 5     # offline baseline epoch order (reading R24)
 
 
 def philox4x32_10(ctr, key):

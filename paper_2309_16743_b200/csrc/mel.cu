@@ -10,11 +10,13 @@
 #include <cstdio>
 #include <cstring>
 #include <ctime>
+#include <future>
 #include <string>
 #include <vector>
 
 #include "../../include/mel.h"
 #include "../../include/mel_ingest.h"
+#include "../../include/mel_dataset.h"
 #include "kernels.h"
 #include "tc_out.h"
 
@@ -69,6 +71,9 @@ struct mel_ctx {
   uint32_t ing_cnt[ING_EVENTS] = {};
   uint32_t ing_head = 0, ing_n = 0;         // FIFO of (event, message count) not yet released
   mel_ingest* ing_handle = nullptr;
+  float* off_buf[2] = {};                   // offline loader: pinned chunk buffers (surrogate_train_offline)
+  uint32_t off_chunk = 0;
+  cudaEvent_t off_ev[2] = {};
   int32_t* d_slots = nullptr;
   bool batch_known = false;        // host knows the last batch size
   uint32_t batch_n = 0;
@@ -843,6 +848,10 @@ void mel_destroy(mel_ctx* c) {
   if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
   for (auto& e : c->ing_ev)
     if (e) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (c->off_buf[i]) cudaFreeHost(c->off_buf[i]);
+    if (c->off_ev[i]) cudaEventDestroy(c->off_ev[i]);
+  }
   if (c->ing_pinned) cudaHostUnregister(c->ing_base);
   if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
   if (c->peer) {
@@ -1087,6 +1096,78 @@ int reservoir_ingest(mel_ctx* c, mel_ingest* g, uint32_t max_msgs, uint32_t time
   }
   if (n_put_host) *n_put_host = n;
   return (eos && n == 0) ? MEL_EOS : MEL_OK;
+}
+
+int surrogate_train_offline(mel_ctx* c, mel_dataset* d, uint64_t seed, uint32_t epoch, uint32_t first_batch,
+                            uint32_t n_batches, double* losses_host, uint32_t* steps_host) {
+  GUARD(c);
+  if (steps_host) *steps_host = 0;
+  if (!d) return fail(c, MEL_EINVAL, "null dataset");
+  if (c->cfg.policy != MEL_FIFO) return fail(c, MEL_EINVAL, "offline training needs mel_config.policy = MEL_FIFO");
+  if (c->cfg.staging_entries < c->B) return fail(c, MEL_EINVAL, "offline training needs staging_entries >= batch");
+  if (mel_dataset_n_field(d) != c->N) return fail(c, MEL_EINVAL, "dataset n_field %u != %u", mel_dataset_n_field(d), c->N);
+  if (c->closed) return fail(c, MEL_ECLOSED, "offline training after reservoir_close");
+  const uint64_t count = mel_dataset_count(d);
+  const uint64_t nb_epoch = count / c->B;                    // the last partial batch is dropped (R24)
+  if (first_batch >= nb_epoch) return MEL_OK;
+  if (n_batches > nb_epoch - first_batch) n_batches = (uint32_t)(nb_epoch - first_batch);
+  std::vector<uint32_t> perm(count);
+  mel_dataset_epoch_order(count, seed, epoch, perm.data());
+  const uint32_t* order = perm.data() + (uint64_t)first_batch * c->B;
+  const uint64_t total = (uint64_t)n_batches * c->B;
+  // records move in chunks through two pinned buffers: the loader threads read chunk q+1
+  // while chunk q's fields are DMA-copied into the staging ring and the GPU trains
+  if (!c->off_buf[0]) {
+    c->off_chunk = c->B < 64 ? c->B : 64;
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaHostAlloc((void**)&c->off_buf[i], (size_t)c->off_chunk * c->N * 4, cudaHostAllocDefault));
+      CK(cudaEventCreateWithFlags(&c->off_ev[i], cudaEventDisableTiming));
+    }
+  }
+  const uint32_t chunk = c->off_chunk;
+  const uint64_t n_chunks = (total + chunk - 1) / chunk;
+  std::vector<uint32_t> sim(2 * chunk), tt(2 * chunk);
+  std::vector<float> X(2 * 5 * chunk);
+  auto load = [&](uint64_t q) {
+    const int b = (int)(q & 1);
+    const uint32_t n = (uint32_t)std::min<uint64_t>(chunk, total - q * chunk);
+    return mel_dataset_read(d, order + q * chunk, n, sim.data() + b * chunk, tt.data() + b * chunk,
+                            X.data() + 5 * b * chunk, c->off_buf[b], c->N);
+  };
+  std::future<int> fut = std::async(std::launch::async, load, (uint64_t)0);
+  uint64_t put = 0;
+  uint32_t steps = 0;
+  uint64_t first_call = c->calls;
+  for (uint64_t q = 0; q < n_chunks; ++q) {
+    const int b = (int)(q & 1);
+    int rl = fut.get();
+    if (rl) return fail(c, MEL_ENOMEM, "dataset read failed (status %d)", rl);
+    if (q + 1 < n_chunks) {
+      CK(cudaEventSynchronize(c->off_ev[b ^ 1]));          // chunk q-1's copies out of that buffer
+      fut = std::async(std::launch::async, load, q + 1);
+    }
+    const uint32_t n = (uint32_t)std::min<uint64_t>(chunk, total - q * chunk);
+    for (uint32_t k = 0; k < n; ++k) {
+      int r = reservoir_put(c, sim[b * chunk + k], tt[b * chunk + k], &X[5 * (b * chunk + k)],
+                            c->off_buf[b] + (uint64_t)k * c->N, 0);
+      if (r) return r;
+      if (++put % c->B == 0) {
+        // the FIFO hands out exactly the B records just put, in epoch order
+        if ((r = reservoir_sample_batch(c, nullptr, nullptr))) return r;
+        if ((r = surrogate_step(c, nullptr))) return r;
+        if (losses_host && steps > 0)
+          if ((r = surrogate_step_result(c, first_call + steps - 1, losses_host + steps - 1, nullptr))) return r;
+        ++steps;
+      }
+    }
+    CK(cudaEventRecord(c->off_ev[b], c->copy_stream));
+  }
+  if (losses_host && steps > 0) {
+    int r = surrogate_step_result(c, first_call + steps - 1, losses_host + steps - 1, nullptr);
+    if (r) return r;
+  }
+  if (steps_host) *steps_host = steps;
+  return MEL_OK;
 }
 
 int reservoir_close(mel_ctx* c) {

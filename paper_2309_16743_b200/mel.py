@@ -36,7 +36,12 @@ EXPORTS = ["mel_config_default", "mel_nccl_unique_id", "mel_create", "mel_destro
            "reservoir_put", "reservoir_close", "reservoir_sample_batch", "surrogate_step", "surrogate_step_result",
            "surrogate_eval",
            "reservoir_stats", "reservoir_dump", "mel_sync", "mel_kernel_time", "mel_kernel_time_reset",
-           "mel_launch_count", "mel_set_flags", "mel_debug_counters", "reservoir_ingest"]
+           "mel_launch_count", "mel_set_flags", "mel_debug_counters", "reservoir_ingest",
+           "surrogate_train_offline"]
+# include/mel_dataset.h (offline baseline data path; host code in libmel.so)
+DATASET_EXPORTS = ["mel_dataset_create", "mel_dataset_append", "mel_dataset_finish", "mel_dataset_open",
+                   "mel_dataset_count", "mel_dataset_n_field", "mel_dataset_epoch_order", "mel_dataset_read",
+                   "mel_dataset_close"]
 # include/mel_ingest.h (host-only ingest channel; in libmel.so and libmel_ingest.so)
 INGEST_EXPORTS = ["mel_ingest_create", "mel_ingest_next", "mel_ingest_release", "mel_ingest_outstanding",
                   "mel_ingest_stats_get", "mel_ingest_segment", "mel_ingest_destroy", "mel_client_open",
@@ -160,6 +165,17 @@ def load_library(path: str = LIB_PATH):
         "mel_set_flags": (C.c_int, [vp, u32]),
         "mel_debug_counters": (C.c_int, [vp, C.POINTER(u64), C.c_int]),
         "reservoir_ingest": (C.c_int, [vp, vp, u32, u32, C.POINTER(u32)]),
+        "surrogate_train_offline": (C.c_int, [vp, vp, u64, u32, u32, u32, C.POINTER(C.c_double), C.POINTER(u32)]),
+        "mel_dataset_create": (C.c_int, [C.c_char_p, u32, C.POINTER(vp)]),
+        "mel_dataset_append": (C.c_int, [vp, u32, u32, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+        "mel_dataset_finish": (C.c_int, [vp]),
+        "mel_dataset_open": (C.c_int, [C.c_char_p, u32, C.POINTER(vp)]),
+        "mel_dataset_count": (u64, [vp]),
+        "mel_dataset_n_field": (u32, [vp]),
+        "mel_dataset_epoch_order": (C.c_int, [u64, u64, u32, C.POINTER(u32)]),
+        "mel_dataset_read": (C.c_int, [vp, C.POINTER(u32), u32, C.POINTER(u32), C.POINTER(u32), C.POINTER(C.c_float),
+                                       C.POINTER(C.c_float), u64]),
+        "mel_dataset_close": (None, [vp]),
     }
     sig.update(_ingest_sigs())
     _bind(lib, sig)
@@ -270,6 +286,17 @@ class Context:
 
     def close(self) -> int:
         return self._check(self.lib.reservoir_close(self.h))
+
+    def train_offline(self, ds: "Dataset", seed: int, epoch: int, first_batch: int = 0, n_batches: int = 1 << 30,
+                      want_losses: bool = True):
+        """surrogate_train_offline: returns (steps, losses or None)."""
+        nb = max(0, min(n_batches, ds.count // self.cfg.batch - first_batch))
+        losses = np.zeros(max(nb, 1), np.float64) if want_losses else None
+        steps = C.c_uint32(0)
+        self._check(self.lib.surrogate_train_offline(
+            self.h, ds.h, seed, epoch, first_batch, n_batches,
+            losses.ctypes.data_as(C.POINTER(C.c_double)) if want_losses else None, C.byref(steps)))
+        return steps.value, (losses[:steps.value] if want_losses else None)
 
     def ingest(self, ing: "Ingest", max_msgs: int = 1 << 30, timeout_us: int = 0):
         """reservoir_ingest: put up to max_msgs first-copy messages of an ingest ring.
@@ -470,3 +497,76 @@ class Client:
         if self.h:
             self.lib.mel_client_close(self.h)
             self.h = C.c_void_p()
+
+
+def _u32p(a):
+    return a.ctypes.data_as(C.POINTER(C.c_uint32))
+
+
+def _f32p(a):
+    return a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def write_dataset(path: str, n_field: int, records) -> int:
+    """mel_dataset_create/append/finish over an iterable of (sim, t, X[5], field fp32)."""
+    lib = load_library()
+    w = C.c_void_p()
+    st = lib.mel_dataset_create(path.encode(), n_field, C.byref(w))
+    if st != OK:
+        raise MelError(st, "mel_dataset_create(%s)" % path)
+    n = 0
+    for sim, t, X, f in records:
+        Xa = np.ascontiguousarray(X, np.float32)
+        fa = np.ascontiguousarray(f, np.float32)
+        st = lib.mel_dataset_append(w, sim, t, _f32p(Xa), _f32p(fa))
+        if st != OK:
+            lib.mel_dataset_finish(w)
+            raise MelError(st, "mel_dataset_append")
+        n += 1
+    st = lib.mel_dataset_finish(w)
+    if st != OK:
+        raise MelError(st, "mel_dataset_finish")
+    return n
+
+
+def epoch_order(count: int, seed: int, epoch: int) -> np.ndarray:
+    perm = np.zeros(count, np.uint32)
+    st = load_library().mel_dataset_epoch_order(count, seed, epoch, _u32p(perm))
+    if st != OK:
+        raise MelError(st, "mel_dataset_epoch_order")
+    return perm
+
+
+class Dataset:
+    """Reader of a file dataset (include/mel_dataset.h) with `threads` loader workers."""
+
+    def __init__(self, path: str, threads: int = 8):
+        self.lib = load_library()
+        self.h = C.c_void_p()
+        st = self.lib.mel_dataset_open(path.encode(), threads, C.byref(self.h))
+        if st != OK:
+            raise MelError(st, "mel_dataset_open(%s)" % path)
+        self.count = int(self.lib.mel_dataset_count(self.h))
+        self.n_field = int(self.lib.mel_dataset_n_field(self.h))
+
+    def read(self, idx, fields: bool = True):
+        idx = np.ascontiguousarray(idx, np.uint32)
+        n = len(idx)
+        sim = np.zeros(n, np.uint32); t = np.zeros(n, np.uint32); X = np.zeros((n, 5), np.float32)
+        F = np.zeros((n, self.n_field), np.float32) if fields else None
+        st = self.lib.mel_dataset_read(self.h, _u32p(idx), n, _u32p(sim), _u32p(t), _f32p(X),
+                                       _f32p(F) if fields else None, self.n_field)
+        if st != OK:
+            raise MelError(st, "mel_dataset_read")
+        return sim, t, X, F
+
+    def close(self):
+        if self.h:
+            self.lib.mel_dataset_close(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -23,7 +23,7 @@ def lib():
 def declared_functions(header=HEADER):
     src = open(header).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    names = re.findall(r"^\s*(?:int|void|uint32_t|const char\*)\s+\**(\w+)\s*\(", src, flags=re.M)
+    names = re.findall(r"^\s*(?:int|void|uint32_t|uint64_t|const char\*)\s+\**(\w+)\s*\(", src, flags=re.M)
     return sorted(set(names))
 
 
@@ -99,3 +99,12 @@ def test_create_fails_loudly_without_gpu(lib):
     from paper_2309_16743_b200 import mel
     with pytest.raises(mel.MelError):
         mel.Context(mel.Config(n_field=100, hidden=(32,), capacity=200, threshold=33, batch=8))
+
+
+def test_dataset_header_exported(lib):
+    """include/mel_dataset.h (offline baseline data path) is exported by libmel.so."""
+    from paper_2309_16743_b200 import mel
+    names = declared_functions(os.path.join(ROOT, "include", "mel_dataset.h"))
+    assert sorted(mel.DATASET_EXPORTS) == names
+    missing = [n for n in names if n not in _exported("libmel.so")]
+    assert not missing, missing
