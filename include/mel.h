@@ -228,6 +228,19 @@ int surrogate_train_offline(mel_ctx* ctx, mel_dataset* ds, uint64_t seed, uint32
                             uint32_t first_batch, uint32_t n_batches, double* losses_host,
                             uint32_t* steps_host);
 
+/* The on-device heat-equation client (include/mel_heat.h): generates the
+ * k time steps u_{X_j}^{t_j} on this GPU from the generator's basis (fp32) and puts
+ * them (reservoir_put with a device field) in order -- generation and training in one
+ * allocation.  X_host [k][5] kelvin, sim_host / t_host [k] (t < tau).  *n_put_host = items
+ * put; MEL_EAGAIN if the staging ring filled first (the rest was not put: sample, then
+ * resubmit from n_put).  MEL_EINVAL if the generator's grid^2 != n_field. */
+#ifndef MEL_HEAT_TYPEDEF_
+#define MEL_HEAT_TYPEDEF_
+typedef struct mel_heat mel_heat;
+#endif
+int reservoir_put_generated(mel_ctx* ctx, mel_heat* gen, const uint32_t* sim_host, const float* X_host,
+                            const uint32_t* t_host, uint32_t k, uint32_t* n_put_host);
+
 /* Signals that reception is over ("When all the simulation data have been
  * generated the blocking related to the threshold is lifted").  Commits pending
  * puts.  A second call returns MEL_EPROTO. */

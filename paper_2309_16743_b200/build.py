@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 OUT = os.path.join(HERE, "libmel.so")
 OBJ = os.path.join(HERE, "build_obj")
-SOURCES = ["mel.cu", "reservoir.cu", "mlp_simt.cu", "tc_out.cu", "ingest.cpp", "dataset.cpp"]
+SOURCES = ["mel.cu", "reservoir.cu", "mlp_simt.cu", "tc_out.cu", "ingest.cpp", "dataset.cpp", "heat.cu"]
 INGEST_OUT = os.path.join(HERE, "libmel_ingest.so")   # host-only, for the simulation clients
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -33,7 +33,7 @@ def nccl_dirs():
 
 def _deps_mtime():
     files = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", f)
-                                                                  for f in ("mel.h", "mel_ingest.h", "mel_dataset.h")]
+                                                                  for f in ("mel.h", "mel_ingest.h", "mel_dataset.h", "mel_heat.h")]
     return max(os.path.getmtime(f) for f in files)
 
 

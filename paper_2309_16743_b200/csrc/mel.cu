@@ -17,6 +17,7 @@
 #include "../../include/mel.h"
 #include "../../include/mel_ingest.h"
 #include "../../include/mel_dataset.h"
+#include "../../include/mel_heat.h"
 #include "kernels.h"
 #include "tc_out.h"
 
@@ -71,6 +72,9 @@ struct mel_ctx {
   uint32_t ing_cnt[ING_EVENTS] = {};
   uint32_t ing_head = 0, ing_n = 0;         // FIFO of (event, message count) not yet released
   mel_ingest* ing_handle = nullptr;
+  float* d_gen = nullptr;                   // on-device client scratch (reservoir_put_generated)
+  float* d_gen_x = nullptr;
+  uint32_t* d_gen_t = nullptr;
   float* off_buf[2] = {};                   // offline loader: pinned chunk buffers (surrogate_train_offline)
   uint32_t off_chunk = 0;
   cudaEvent_t off_ev[2] = {};
@@ -1167,6 +1171,45 @@ int surrogate_train_offline(mel_ctx* c, mel_dataset* d, uint64_t seed, uint32_t 
     if (r) return r;
   }
   if (steps_host) *steps_host = steps;
+  return MEL_OK;
+}
+
+int reservoir_put_generated(mel_ctx* c, mel_heat* h, const uint32_t* sim, const float* X, const uint32_t* t,
+                            uint32_t k, uint32_t* n_put_host) {
+  GUARD(c);
+  if (n_put_host) *n_put_host = 0;
+  if (!h || !sim || !X || !t) return fail(c, MEL_EINVAL, "null generator argument");
+  const uint32_t n = mel_heat_grid(h);
+  if ((uint64_t)n * n != c->N) return fail(c, MEL_EINVAL, "generator grid %u^2 != n_field %u", n, c->N);
+  if (c->closed) return fail(c, MEL_ECLOSED, "reservoir_put_generated after reservoir_close");
+  const uint32_t kmax = 64;
+  if (!c->d_gen) {
+    DALLOC(c->d_gen, (size_t)kmax * c->N);
+    DALLOC(c->d_gen_x, (size_t)kmax * 5);
+    DALLOC(c->d_gen_t, kmax);
+  }
+  uint32_t done = 0;
+  while (done < k) {
+    const uint32_t m = std::min(kmax, k - done);
+    for (uint32_t j = 0; j < m; ++j)
+      if (t[done + j] >= mel_heat_tau(h)) return fail(c, MEL_EINVAL, "t = %u >= tau", t[done + j]);
+    // the previous chunk's D2D copies out of the scratch are ordered before this on c->stream
+    CK(cudaMemcpyAsync(c->d_gen_x, X + 5ull * done, 20ull * m, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_gen_t, t + done, 4ull * m, cudaMemcpyHostToDevice, c->stream));
+    if (mel_heat_fields(h, c->d_gen_x, c->d_gen_t, m, c->d_gen, c->stream) != 0)
+      return fail(c, MEL_ECUDA, "heat field generation failed");
+    c->launches += 1;
+    for (uint32_t j = 0; j < m; ++j) {
+      int r = reservoir_put(c, sim[done + j], t[done + j], X + 5ull * (done + j), c->d_gen + (uint64_t)j * c->N, 1);
+      if (r == MEL_EAGAIN) {
+        if (n_put_host) *n_put_host = done + j;
+        return MEL_EAGAIN;
+      }
+      if (r) return r;
+    }
+    done += m;
+  }
+  if (n_put_host) *n_put_host = done;
   return MEL_OK;
 }
 

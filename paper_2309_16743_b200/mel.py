@@ -37,7 +37,10 @@ EXPORTS = ["mel_config_default", "mel_nccl_unique_id", "mel_create", "mel_destro
            "surrogate_eval",
            "reservoir_stats", "reservoir_dump", "mel_sync", "mel_kernel_time", "mel_kernel_time_reset",
            "mel_launch_count", "mel_set_flags", "mel_debug_counters", "reservoir_ingest",
-           "surrogate_train_offline"]
+           "surrogate_train_offline", "reservoir_put_generated"]
+# include/mel_heat.h (on-device heat-equation client)
+HEAT_EXPORTS = ["mel_heat_create", "mel_heat_basis_bytes", "mel_heat_grid", "mel_heat_tau", "mel_heat_fields",
+                "mel_heat_destroy"]
 # include/mel_dataset.h (offline baseline data path; host code in libmel.so)
 DATASET_EXPORTS = ["mel_dataset_create", "mel_dataset_append", "mel_dataset_finish", "mel_dataset_open",
                    "mel_dataset_count", "mel_dataset_n_field", "mel_dataset_epoch_order", "mel_dataset_read",
@@ -176,6 +179,14 @@ def load_library(path: str = LIB_PATH):
         "mel_dataset_read": (C.c_int, [vp, C.POINTER(u32), u32, C.POINTER(u32), C.POINTER(u32), C.POINTER(C.c_float),
                                        C.POINTER(C.c_float), u64]),
         "mel_dataset_close": (None, [vp]),
+        "reservoir_put_generated": (C.c_int, [vp, vp, C.POINTER(u32), C.POINTER(C.c_float), C.POINTER(u32), u32,
+                                              C.POINTER(u32)]),
+        "mel_heat_create": (C.c_int, [u32, u32, C.c_double, C.c_double, C.c_double, C.POINTER(vp)]),
+        "mel_heat_basis_bytes": (u64, [vp]),
+        "mel_heat_grid": (u32, [vp]),
+        "mel_heat_tau": (u32, [vp]),
+        "mel_heat_fields": (C.c_int, [vp, vp, vp, u32, vp, vp]),
+        "mel_heat_destroy": (None, [vp]),
     }
     sig.update(_ingest_sigs())
     _bind(lib, sig)
@@ -286,6 +297,17 @@ class Context:
 
     def close(self) -> int:
         return self._check(self.lib.reservoir_close(self.h))
+
+    def put_generated(self, gen: "Heat", sims, X, t):
+        """reservoir_put_generated: fields made on this GPU by the heat client; returns
+        (status, n_put)."""
+        sims = np.ascontiguousarray(sims, np.uint32)
+        Xa = np.ascontiguousarray(X, np.float32).reshape(-1, 5)
+        ta = np.ascontiguousarray(t, np.uint32)
+        n = C.c_uint32(0)
+        st = self._check(self.lib.reservoir_put_generated(self.h, gen.h, _u32p(sims), _f32p(Xa), _u32p(ta), len(ta),
+                                                          C.byref(n)), (OK, EAGAIN))
+        return st, n.value
 
     def train_offline(self, ds: "Dataset", seed: int, epoch: int, first_batch: int = 0, n_batches: int = 1 << 30,
                       want_losses: bool = True):
@@ -568,5 +590,42 @@ class Dataset:
     def __del__(self):
         try:
             self.close()
+        except Exception:
+            pass
+
+
+class Heat:
+    """The on-device heat-equation client (include/mel_heat.h): builds the fp64 basis on
+    the current GPU; fields(X, t) -> fp32 device fields (torch tensors)."""
+
+    def __init__(self, n: int, tau: int, alpha: float = 1.0, dt: float = 0.01, length: float = 1.0):
+        self.lib = load_library()
+        self.h = C.c_void_p()
+        st = self.lib.mel_heat_create(n, tau, alpha, dt, length, C.byref(self.h))
+        if st != OK:
+            raise MelError(st, "mel_heat_create(%d, %d)" % (n, tau))
+        self.n, self.tau = n, tau
+        self.basis_bytes = int(self.lib.mel_heat_basis_bytes(self.h))
+
+    def fields(self, X, t, stream=None):
+        import torch
+        X = torch.as_tensor(X, dtype=torch.float32, device="cuda").reshape(-1, 5).contiguous()
+        t = torch.as_tensor(t, dtype=torch.int32, device="cuda").contiguous()
+        out = torch.empty((X.shape[0], self.n * self.n), dtype=torch.float32, device="cuda")
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        st = self.lib.mel_heat_fields(self.h, C.c_void_p(X.data_ptr()), C.c_void_p(t.data_ptr()), X.shape[0],
+                                      C.c_void_p(out.data_ptr()), C.c_void_p(s))
+        if st != OK:
+            raise MelError(st, "mel_heat_fields")
+        return out
+
+    def destroy(self):
+        if self.h:
+            self.lib.mel_heat_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.destroy()
         except Exception:
             pass

@@ -108,3 +108,12 @@ def test_dataset_header_exported(lib):
     assert sorted(mel.DATASET_EXPORTS) == names
     missing = [n for n in names if n not in _exported("libmel.so")]
     assert not missing, missing
+
+
+def test_heat_header_exported(lib):
+    """include/mel_heat.h (on-device heat-equation client) is exported by libmel.so."""
+    from paper_2309_16743_b200 import mel
+    names = declared_functions(os.path.join(ROOT, "include", "mel_heat.h"))
+    assert sorted(mel.HEAT_EXPORTS) == names
+    missing = [n for n in names if n not in _exported("libmel.so")]
+    assert not missing, missing
