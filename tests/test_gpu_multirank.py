@@ -32,3 +32,18 @@ def test_multi_rank_parity(world, mode):
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
     assert r.stdout.count("replicas identical") == world
+
+
+@pytest.mark.parametrize("world", [2])
+def test_multi_rank_ingest(world):
+    """Client processes -> per-rank shared-memory rings (round robin from the client id)
+    -> reservoir_ingest on every rank -> collective training (tests/mp_gpu_ingest.py)."""
+    if _ngpu() < world:
+        pytest.skip("needs %d GPUs" % world)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=%d" % world,
+           "--master-addr=127.0.0.1", "--master-port=%d" % (29300 + os.getpid() % 300),
+           os.path.join(HERE, "mp_gpu_ingest.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0
+    assert r.stdout.count("replicas identical") == world
