@@ -279,7 +279,12 @@ def main():
     with Clocks(local) as clk:
         torch.cuda.nvtx.range_push("timed")
         ev0.record(stream)
+        win_ev = []                                 # throughput over windows of 10 steps
         for i in range(args.warmup, total_steps):
+            if (i - args.warmup) % 10 == 0 and i > args.warmup:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(stream)
+                win_ev.append(e)
             one_step(i)
         ev1.record(stream)
         torch.cuda.nvtx.range_pop()
@@ -398,6 +403,22 @@ def main():
             kernels[name]["frac"] = f2[b2][0] / f2[b2][1]
     step_flops = (6.0 * B * n_field * K + 6.0 * B * K * K + 4.0 * B * 6 * K)
     tensor_frac_step = step_flops / (ms_step / 1e3) / 1e12 / P["bf16_tflops"]
+    # the step's tensor fraction vs the burst and the sustained peak,
+    # and vs the attainable min(peak, I x HBM) of the ideal fused step (I = FLOP / ideal bytes:
+    # bf16 targets B*N*2, two reads of the bf16 W_L shadow, 26 B/param of fused Adam)
+    ideal_bytes = B * n_field * 2.0 + 2.0 * (K * n_field * 2.0) + 26.0 * n_params
+    intensity = step_flops / ideal_bytes
+    attainable = min(P["bf16_tflops"], intensity * P["hbm_gbs"] / 1e3)
+    step_tflops = step_flops / (ms_step / 1e3) / 1e12
+    tensor_roofline = {"step_tflops": step_tflops, "frac_burst": tensor_frac_step,
+                       "frac_sustained": step_tflops / P.get("bf16_tflops_sustained", P["bf16_tflops"]),
+                       "intensity_flop_per_byte": intensity, "attainable_tflops": attainable,
+                       "frac_attainable": step_tflops / attainable}
+    windows = None
+    if len(win_ev) >= 2:
+        w = [win_ev[j].elapsed_time(win_ev[j + 1]) for j in range(len(win_ev) - 1)]
+        w = [B * world * 10 / (x / 1e3) for x in w]
+        windows = {"steps_per_window": 10, "n": len(w), "mean": float(np.mean(w)), "median": float(np.median(w))}
 
     # ---- end-to-end through the public API with host buffers ----
     e2e = None
@@ -456,7 +477,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (exact heat-equation solutions, seeded)",
             "config": config_block(args, world), "gpu_launches": launches, "clocks": clk.summary(),
-            "roofline": roofline, "tensor_frac_step": tensor_frac_step, "kernels": kernels,
+            "roofline": roofline, "tensor_frac_step": tensor_frac_step, "tensor_roofline": tensor_roofline,
+            "windows_samples_per_s": windows, "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e, "val_mse": val,
             "reservoir": {"population": stats["population"], "unseen": stats["unseen"],
                           "evictions": stats["evictions"], "puts": stats["puts"], "draws": stats["draws"],
