@@ -188,7 +188,9 @@ int mel_set_state(mel_ctx* ctx, const mel_state_view* in);
  * is committed to a slot at the next commit point (start of
  * reservoir_sample_batch, or reservoir_close).  field_on_device = 0: field is
  * host memory, copied before return (pinned memory makes the copy asynchronous);
- * 1: device pointer, copied in stream order.  Errors: MEL_ECLOSED after close,
+ * 1: device pointer, read in stream order by the commit that consumes the item -- zero
+ * copy when it is 16-byte aligned and n_field % 4 == 0, else copied on the stream at the
+ * call; either way it must stay valid and unchanged until the next mel_sync().  Errors: MEL_ECLOSED after close,
  * MEL_EAGAIN when the staging ring is full (the caller retries after sampling),
  * MEL_EINVAL. */
 int reservoir_put(mel_ctx* ctx, uint32_t sim_id, uint32_t t, const float X_host[5],

@@ -80,6 +80,8 @@ struct ResArgs {
   uint32_t rank;
   uint2* plan;               // [S] (entry, slot)
   uint32_t policy;           // 0 Reservoir, 1 FIFO, 2 FIRO (mel_policy)
+  const float* const* st_src;  // [S] mapped: the caller's device field of a zero-copy put, else null
+  const float** plan_src;      // [S] the source field of plan entry i (null: the staging ring)
 };
 
 // reservoir.cu

@@ -55,6 +55,7 @@ struct mel_ctx {
   Mirror* h_mirror = nullptr;
   Mirror* d_mirror = nullptr;
   StMeta* h_stmeta = nullptr;      // pinned ring mirror of staging metadata
+  const float** h_stsrc = nullptr; // pinned [S]: a zero-copy device put's field, else null
   uint64_t tail = 0;               // accepted puts
   uint64_t known_consumed = 0;
   bool copy_fence = false;                  // see ensure_ring_space
@@ -732,6 +733,14 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
     a.payload = pl;
   }
   DALLOC(a.plan, S);
+  DALLOC(a.plan_src, S);
+  CK(cudaHostAlloc((void**)&c->h_stsrc, sizeof(float*) * S, cudaHostAllocMapped));
+  memset(c->h_stsrc, 0, sizeof(float*) * S);
+  {
+    const float** d_stsrc;
+    CK(cudaHostGetDevicePointer((void**)&d_stsrc, c->h_stsrc, 0));
+    a.st_src = d_stsrc;
+  }
   a.st = c->d_st; a.mirror = c->d_mirror; a.st_meta = d_stmeta; a.st_field = d_stfield; a.S = S;
   a.C = C; a.theta = g->threshold; a.Npad = c->Npad; a.N = c->N; a.storage = (int)g->storage;
   a.lo = g->temp_lo; a.span = g->temp_hi - g->temp_lo; a.seed = g->seed; a.rank = (uint32_t)c->rank;
@@ -882,12 +891,14 @@ void mel_destroy(mel_ctx* c) {
                   c->d_shadow[0], c->d_shadow[1], c->d_xn, c->d_z[0], c->d_z[1], c->d_h[0], c->d_h[1], c->d_dz[0],
                   c->d_dz[1], c->d_dy, c->d_part, c->d_sse_part, c->d_sd, c->d_eval_x, c->d_eval_t, c->d_eval_y,
                   c->d_eval_f, c->d_eval_z[0], c->d_eval_z[1], c->d_eval_h[0], c->d_eval_h[1], c->d_eval_xn,
-                  c->d_acc, c->d_cnt};
+                  c->d_acc, c->d_cnt, c->d_gen, c->d_gen_x, c->d_gen_t};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   tc::free_buffers(c->tcb);
   if (c->h_mirror) cudaFreeHost(c->h_mirror);
   if (c->h_stmeta) cudaFreeHost(c->h_stmeta);
+  if (c->h_stsrc) cudaFreeHost(c->h_stsrc);
+  if (c->ra.plan_src) cudaFree(c->ra.plan_src);
   if (c->ev_copy) cudaEventDestroy(c->ev_copy);
   if (c->ev_fence) cudaEventDestroy(c->ev_fence);
   for (int i = 0; i < MEL_RESULT_RING; ++i)
@@ -990,7 +1001,15 @@ int mel_set_state(mel_ctx* c, const mel_state_view* s) {
   return MEL_OK;
 }
 
+static int put_impl(mel_ctx* c, uint32_t sim, uint32_t t, const float X[5], const float* field, int on_device,
+                    bool zero_copy);
+
 int reservoir_put(mel_ctx* c, uint32_t sim, uint32_t t, const float X[5], const float* field, int on_device) {
+  return put_impl(c, sim, t, X, field, on_device, true);
+}
+
+static int put_impl(mel_ctx* c, uint32_t sim, uint32_t t, const float X[5], const float* field, int on_device,
+                    bool zero_copy) {
   GUARD(c);
   if (!X || !field) return fail(c, MEL_EINVAL, "null X or field");
   if (c->closed) return fail(c, MEL_ECLOSED, "reservoir_put after reservoir_close");
@@ -1005,7 +1024,12 @@ int reservoir_put(mel_ctx* c, uint32_t sim, uint32_t t, const float X[5], const 
   // rewritten after that commit published its progress (ensure_ring_space)
   c->h_stmeta[e] = m;
   float* dst = const_cast<float*>(c->ra.st_field) + (uint64_t)e * c->Npad;
-  if (on_device) {
+  c->h_stsrc[e] = nullptr;
+  if (on_device && zero_copy && c->N % 4 == 0 && ((uintptr_t)field & 15) == 0) {
+    // zero copy: the commit that consumes this entry reads the caller's field in stream
+    // order (the mel.h contract keeps it valid until the next mel_sync)
+    c->h_stsrc[e] = field;
+  } else if (on_device) {
     CK(cudaMemcpyAsync(dst, field, 4ull * c->N, cudaMemcpyDeviceToDevice, c->stream));
   } else {
     if (c->copy_fence) {
@@ -1200,7 +1224,8 @@ int reservoir_put_generated(mel_ctx* c, mel_heat* h, const uint32_t* sim, const 
       return fail(c, MEL_ECUDA, "heat field generation failed");
     c->launches += 1;
     for (uint32_t j = 0; j < m; ++j) {
-      int r = reservoir_put(c, sim[done + j], t[done + j], X + 5ull * (done + j), c->d_gen + (uint64_t)j * c->N, 1);
+      // the scratch is reused by the next chunk before this entry's commit: copy it
+      int r = put_impl(c, sim[done + j], t[done + j], X + 5ull * (done + j), c->d_gen + (uint64_t)j * c->N, 1, false);
       if (r == MEL_EAGAIN) {
         if (n_put_host) *n_put_host = done + j;
         return MEL_EAGAIN;

@@ -69,6 +69,7 @@ __device__ void commit_queue(const ResArgs& a, uint64_t tail, uint32_t closed) {
     a.seen[j] = 0;
     a.put_seq[j] = q + i;
     a.plan[i] = make_uint2(e, j);
+    a.plan_src[i] = a.st_src[e];
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -166,6 +167,7 @@ commit_ctrl(ResArgs a, uint64_t tail, uint32_t closed) {
     a.seen[j] = 0;
     a.put_seq[j] = q0 + i;
     a.plan[i] = make_uint2(ej.x, j);
+    a.plan_src[i] = a.st_src[ej.x];
   }
   if (threadIdx.x == 0) st->evictions += s_nev;
   __syncthreads();
@@ -185,12 +187,14 @@ __global__ void __launch_bounds__(256)
 commit_copy(ResArgs a) {
   pdl_enter();
   // a fixed grid strides over every committed entry (the host only knows an upper bound
-  // on their number): 16-byte loads of the staged fp32 field, normalised on the fly
+  // on their number): 16-byte loads of the staged fp32 field (or, for a device put, of the
+  // caller's own field: no staging copy), normalised on the fly
   const uint32_t n_plan = a.st->n_plan;
   const uint32_t n4 = (a.N + 3) / 4;
   for (uint32_t y = 0; y < n_plan; ++y) {
     const uint2 ej = a.plan[y];
-    const float4* src = reinterpret_cast<const float4*>(a.st_field + (uint64_t)ej.x * a.Npad);
+    const float* zc = a.plan_src[y];              // zero-copy device put: read the caller's field
+    const float4* src = reinterpret_cast<const float4*>(zc ? zc : a.st_field + (uint64_t)ej.x * a.Npad);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
       float4 v = __ldg(src + i);
       float o[4] = {v.x, v.y, v.z, v.w};
