@@ -105,7 +105,11 @@ def test_random_schedules_with_backpressure_and_ring_wrap(mel, seed):
     assert e.value.code == mel.EPROTO
 
 
-def test_device_resident_puts_match_host_puts(mel):
+@pytest.mark.parametrize("offset", [0, 1], ids=["zero-copy", "unaligned-copied"])
+def test_device_resident_puts_match_host_puts(mel, offset):
+    """Device puts: an aligned field is read by the commit straight from the caller's
+    buffer (zero copy); a 4-byte-offset one is copied at the call.  Both must equal the
+    host puts bit for bit."""
     import torch
     wl = design.TINY_EVICT
     table = FieldTable(wl)
@@ -115,9 +119,11 @@ def test_device_resident_puts_match_host_puts(mel):
     for (s, t) in design.stream_order(wl.sims, wl.tau)[:60]:
         f = table.field(s, t)
         a.put(s, t, table.Xs(s), f)
-        keep.append(torch.from_numpy(f).cuda())
+        buf = torch.zeros(len(f) + offset, dtype=torch.float32, device="cuda")
+        buf[offset:] = torch.from_numpy(f).cuda()
+        keep.append(buf)
         torch.cuda.synchronize()
-        b.put(s, t, table.Xs(s), keep[-1])
+        b.put(s, t, table.Xs(s), buf[offset:])
         if t % 5 == 4:
             assert list(a.sample(True)[1]) == list(b.sample(True)[1])
     da, db = a.dump(), b.dump()
