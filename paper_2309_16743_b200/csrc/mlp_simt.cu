@@ -306,15 +306,6 @@ __device__ __forceinline__ void store_shadow(__nv_bfloat16* shadow, uint64_t e, 
   }
 }
 
-__device__ __forceinline__ float4 ld_stream(const float4* p) {
-  float4 r;
-  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ void st_stream(float4* p, const float4& v) {
-  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
-}
-
 // UNR float4 of each array in flight per thread; the tail loop handles the rest
 template <int UNR>
 __global__ void __launch_bounds__(256)
