@@ -1500,6 +1500,43 @@ int reservoir_dump(mel_ctx* c, uint32_t* sim, uint32_t* t, float* X, uint32_t* s
   return MEL_OK;
 }
 
+int mel_params_copy(mel_ctx* dst, mel_ctx* src) {
+  GUARD(src);
+  mel_ctx* c = src;                               // errors are reported on (and poison) src
+  if (!dst || dst == src) return fail(src, MEL_EINVAL, "bad destination context");
+  if (dst->poisoned) return dst->poisoned;
+  if (dst->n_flat != src->n_flat || dst->L != src->L || dst->N != src->N || dst->Npad != src->Npad)
+    return fail(src, MEL_EINVAL, "parameter layouts differ");
+  for (int l = 0; l < src->L; ++l)
+    if (dst->dims[l] != src->dims[l]) return fail(src, MEL_EINVAL, "parameter layouts differ");
+  int r = gather_master(src, false);              // full fp32 W_L on src (collective under ZeRO)
+  if (r) return r;
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, src->dev, dst->dev) == cudaSuccess && can) {
+    // direct NVLink copy engine path (otherwise the driver stages through host memory)
+    cudaError_t e = cudaDeviceEnablePeerAccess(dst->dev, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return fail(c, MEL_ECUDA, "peer access: %s",
+                                                                                 cudaGetErrorString(e));
+    (void)cudaGetLastError();
+  }
+  cudaEvent_t ready, copied;
+  CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  CK(cudaEventRecord(ready, src->stream));
+  cudaSetDevice(dst->dev);
+  CK(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+  CK(cudaStreamWaitEvent(dst->stream, ready, 0));
+  CK(cudaMemcpyPeerAsync(dst->d_p, dst->dev, src->d_p, src->dev, 4ull * src->n_flat, dst->stream));
+  CK(cudaEventRecord(copied, dst->stream));
+  r = refresh_shadow(dst);
+  if (r) return r;
+  cudaSetDevice(src->dev);
+  // src's next update of its parameters waits until they have been read
+  CK(cudaStreamWaitEvent(src->stream, copied, 0));
+  cudaEventDestroy(ready);
+  cudaEventDestroy(copied);
+  return MEL_OK;
+}
+
 int mel_sync(mel_ctx* c) {
   GUARD(c);
   if (c->comm_stream) CK(cudaStreamSynchronize(c->comm_stream));

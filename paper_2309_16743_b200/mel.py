@@ -37,7 +37,7 @@ EXPORTS = ["mel_config_default", "mel_nccl_unique_id", "mel_create", "mel_destro
            "surrogate_eval",
            "reservoir_stats", "reservoir_dump", "mel_sync", "mel_kernel_time", "mel_kernel_time_reset",
            "mel_launch_count", "mel_set_flags", "mel_debug_counters", "reservoir_ingest",
-           "surrogate_train_offline", "reservoir_put_generated"]
+           "surrogate_train_offline", "reservoir_put_generated", "mel_params_copy"]
 # include/mel_heat.h (on-device heat-equation client)
 HEAT_EXPORTS = ["mel_heat_create", "mel_heat_basis_bytes", "mel_heat_grid", "mel_heat_tau", "mel_heat_fields",
                 "mel_heat_destroy"]
@@ -179,6 +179,7 @@ def load_library(path: str = LIB_PATH):
         "mel_dataset_read": (C.c_int, [vp, C.POINTER(u32), u32, C.POINTER(u32), C.POINTER(u32), C.POINTER(C.c_float),
                                        C.POINTER(C.c_float), u64]),
         "mel_dataset_close": (None, [vp]),
+        "mel_params_copy": (C.c_int, [vp, vp]),
         "reservoir_put_generated": (C.c_int, [vp, vp, C.POINTER(u32), C.POINTER(C.c_float), C.POINTER(u32), u32,
                                               C.POINTER(u32)]),
         "mel_heat_create": (C.c_int, [u32, u32, C.c_double, C.c_double, C.c_double, C.POINTER(vp)]),
@@ -297,6 +298,13 @@ class Context:
 
     def close(self) -> int:
         return self._check(self.lib.reservoir_close(self.h))
+
+    def copy_params_from(self, src: "Context"):
+        """mel_params_copy(self, src): src's parameters into this context (another GPU),
+        asynchronous on both streams."""
+        st = self.lib.mel_params_copy(self.h, src.h)
+        if st != OK:
+            raise MelError(st, self.lib.mel_last_error(src.h).decode(errors="replace"))
 
     def put_generated(self, gen: "Heat", sims, X, t):
         """reservoir_put_generated: fields made on this GPU by the heat client; returns

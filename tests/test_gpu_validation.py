@@ -1,0 +1,53 @@
+"""Validation on a dedicated GPU: mel_params_copy moves the
+trainer's parameters to a context on another GPU, whose surrogate_eval then matches the
+trainer's own evaluation bit for bit, and the trainer can keep stepping meanwhile."""
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+from harness import FieldTable, make_config
+from mel_inputs import design, heat
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mel():
+    from paper_2309_16743_b200 import build, mel as m
+    build.build()
+    return m
+
+
+def test_params_copy_to_a_second_gpu(mel):
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    wl = replace(design.MEDIUM, n=32, sims=12, capacity=400, threshold=60, batch=64, puts_per_step=40)
+    table = FieldTable(wl)
+    cfg = make_config(wl, precision=mel.BF16, storage=mel.STORE_BF16)
+    trainer = mel.Context(cfg, device=0)
+    val = mel.Context(cfg, device=1)
+    order = design.stream_order(wl.sims, wl.tau)
+    pos = [0]
+
+    def train(k):
+        for _ in range(k):
+            for s, t in order[pos[0]:pos[0] + wl.puts_per_step]:
+                trainer.put(s, t, table.Xs(s), table.field(s, t))
+            pos[0] += wl.puts_per_step
+            trainer.sample()
+            trainer.step(want_loss=False)
+
+    Xv = design.draw_design(3, seed=1, validation=True)
+    X = np.repeat(Xv, wl.tau, 0).astype(np.float32)
+    t = np.tile(np.arange(wl.tau), 3).astype(np.uint32)
+    F = np.concatenate([heat.simulate(Xv[s], wl.n, wl.tau) for s in range(3)])
+    train(8)
+    val.copy_params_from(trainer)
+    train(3)                                   # the copy does not block the trainer's queue
+    assert np.isfinite(val.eval(X, t, F)[0])
+    val.copy_params_from(trainer)
+    a, b = trainer.get_params(), val.get_params()
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
+    assert trainer.eval(X, t, F)[0] == val.eval(X, t, F)[0]
