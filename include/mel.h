@@ -276,7 +276,9 @@ int surrogate_step(mel_ctx* ctx, double* loss_host);
 int surrogate_step_result(mel_ctx* ctx, uint64_t call, double* loss_host, int* status_host);
 
 /* Forward-only validation of n samples given on the host: X_host n x 5
- * kelvin, t_host n, fields_host n x N fp32 kelvin (nullable: then no MSE).
+ * kelvin, t_host n, fields_host n x N fp32 kelvin (nullable: then no MSE; it may also
+ * point into this context's GPU memory -- told apart by unified addressing -- and is then
+ * read in place instead of copied from the host).
  * mse_host (nullable) receives the MSE in normalised units (reading Q13);
  * pred_host (nullable, n x N) the predictions de-normalised to kelvin.
  * Synchronises; COLLECTIVE with world > 1 in bf16 mode (gathers the W_L master). */

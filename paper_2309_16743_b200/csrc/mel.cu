@@ -1421,6 +1421,16 @@ int surrogate_eval(mel_ctx* c, const float* X, const uint32_t* t, const float* f
   DALLOC(d_part, 256);
   double total = 0.0;
   const float lo = c->cfg.temp_lo, span = c->cfg.temp_hi - c->cfg.temp_lo;
+  // held-out fields already in this GPU's memory (unified addressing tells) are read in
+  // place instead of being copied from the host
+  bool fields_dev = false;
+  if (fields) {
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, fields) == cudaSuccess)
+      fields_dev = (pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged) && pa.device == c->dev;
+    else
+      (void)cudaGetLastError();
+  }
   std::vector<double> parts(256);
   for (uint32_t s0 = 0; s0 < n; s0 += chunk) {
     const uint32_t m = (n - s0) < chunk ? (n - s0) : chunk;
@@ -1433,8 +1443,13 @@ int surrogate_eval(mel_ctx* c, const float* X, const uint32_t* t, const float* f
           (int)c->Klast, c->d_eval_y, (int)c->Npad, EPI_BIAS, c->d_p + c->off[2 * (L - 1) + 1], nullptr, 0, 1, c->stream);
     c->launches += 2 + (L - 1) + 1;
     if (fields) {
-      CK(cudaMemcpyAsync(c->d_eval_f, fields + (uint64_t)s0 * c->N, 4ull * m * c->N, cudaMemcpyHostToDevice, c->stream));
-      normalise_fields(c->d_eval_f, c->d_eval_f, (uint64_t)m * c->N, lo, span, c->stream);
+      if (fields_dev) {
+        normalise_fields(fields + (uint64_t)s0 * c->N, c->d_eval_f, (uint64_t)m * c->N, lo, span, c->stream);
+      } else {
+        CK(cudaMemcpyAsync(c->d_eval_f, fields + (uint64_t)s0 * c->N, 4ull * m * c->N, cudaMemcpyHostToDevice,
+                           c->stream));
+        normalise_fields(c->d_eval_f, c->d_eval_f, (uint64_t)m * c->N, lo, span, c->stream);
+      }
       const int np = eval_mse_partial(c->d_eval_y, c->d_eval_f, (int)m, (int)c->N, (int)c->Npad, d_part, c->stream);
       c->launches += 2;
       CK(cudaMemcpyAsync(parts.data(), d_part, 8ull * np, cudaMemcpyDeviceToHost, c->stream));

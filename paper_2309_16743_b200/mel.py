@@ -363,11 +363,17 @@ class Context:
         X = np.ascontiguousarray(X, dtype=np.float32)
         t = np.ascontiguousarray(t, dtype=np.uint32)
         n = X.shape[0]
-        f = np.ascontiguousarray(fields, dtype=np.float32) if fields is not None else None
+        if fields is not None and hasattr(fields, "data_ptr"):      # torch tensor (device or host)
+            fields = fields.float().contiguous()
+            fptr = C.cast(C.c_void_p(fields.data_ptr()), C.POINTER(C.c_float))
+            f = None
+        else:
+            f = np.ascontiguousarray(fields, dtype=np.float32) if fields is not None else None
+            fptr = _fptr(f) if f is not None else None
         pred = np.zeros((n, self.cfg.n_field), dtype=np.float32) if want_pred else None
         mse = C.c_double()
         self._check(self.lib.surrogate_eval(self.h, _fptr(X), t.ctypes.data_as(C.POINTER(C.c_uint32)),
-                                            _fptr(f) if f is not None else None, n, C.byref(mse),
+                                            fptr, n, C.byref(mse),
                                             _fptr(pred) if want_pred else None))
         return mse.value, pred
 

@@ -51,3 +51,23 @@ def test_params_copy_to_a_second_gpu(mel):
     a, b = trainer.get_params(), val.get_params()
     assert all(np.array_equal(x, y) for x, y in zip(a, b))
     assert trainer.eval(X, t, F)[0] == val.eval(X, t, F)[0]
+
+
+def test_eval_reads_device_fields_in_place(mel):
+    """surrogate_eval with the held-out fields already on the GPU (unified addressing)
+    gives the same MSE as with the fields in host memory."""
+    import torch
+    wl = replace(design.MEDIUM, n=32, sims=12, capacity=400, threshold=60, batch=64, puts_per_step=40)
+    table = FieldTable(wl)
+    ctx = mel.Context(make_config(wl, precision=mel.BF16, storage=mel.STORE_BF16), device=0)
+    for s, t in design.stream_order(wl.sims, wl.tau)[:200]:
+        ctx.put(s, t, table.Xs(s), table.field(s, t))
+    ctx.sample()
+    ctx.step(want_loss=False)
+    Xv = design.draw_design(3, seed=1, validation=True)
+    X = np.repeat(Xv, wl.tau, 0).astype(np.float32)
+    t = np.tile(np.arange(wl.tau), 3).astype(np.uint32)
+    F = np.concatenate([heat.simulate(Xv[s], wl.n, wl.tau) for s in range(3)])
+    m_host, _ = ctx.eval(X, t, F)
+    m_dev, _ = ctx.eval(X, t, torch.from_numpy(F).cuda(0))
+    assert m_host == m_dev and np.isfinite(m_host)

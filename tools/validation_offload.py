@@ -2,7 +2,8 @@
 f4), paper shape: train S steps with a validation pass on the 10 held-out simulations
 every V steps, (a) inline on the training GPU, (b) offloaded: mel_params_copy to a second
 GPU's context and surrogate_eval there from a helper thread while training continues.
-One JSON line: wall time and training samples/s of both, validation MSEs."""
+One JSON line per placement of the held-out fields (host memory, or resident on the GPU
+that evaluates): wall time and training samples/s of both, validation MSEs."""
 import argparse
 import json
 import os
@@ -33,13 +34,16 @@ def main():
     phi = heat_torch.basis(grid, tau, device=dev)
     Xv = torch.from_numpy(design.draw_design(10, seed=1, validation=True)).to(dev)
     tv = torch.arange(tau, device=dev).repeat(10)
-    Fv = heat_torch.fields(phi, Xv.repeat_interleave(tau, 0), tv).cpu().numpy()
+    Fv_dev = heat_torch.fields(phi, Xv.repeat_interleave(tau, 0), tv)        # held-out fields, GPU 0
+    Fv = Fv_dev.cpu().numpy()
     Xv_np, tv_np = Xv.repeat_interleave(tau, 0).cpu().numpy(), tv.cpu().numpy().astype(np.uint32)
     sims = 200
     Xd = torch.from_numpy(design.draw_design(sims, seed=1)).to(dev)
     order = design.stream_order(sims, tau)
 
-    def run(offload):
+    Fv_dev1 = Fv_dev.to(torch.device("cuda", 1))                             # ... and on GPU 1
+
+    def run(offload, device_fields):
         ctx = mel.Context(cfg, device=0)
         val = mel.Context(cfg, device=1) if offload else None
         sent = 0
@@ -63,11 +67,12 @@ def main():
             if (k + 1) % a.every == 0:
                 if offload:
                     val.copy_params_from(ctx)
-                    th = threading.Thread(target=lambda: mses.append(val.eval(Xv_np, tv_np, Fv)[0]))
+                    fv = Fv_dev1 if device_fields else Fv
+                    th = threading.Thread(target=lambda: mses.append(val.eval(Xv_np, tv_np, fv)[0]))
                     th.start()
                     threads.append(th)
                 else:
-                    mses.append(ctx.eval(Xv_np, tv_np, Fv)[0])
+                    mses.append(ctx.eval(Xv_np, tv_np, Fv_dev if device_fields else Fv)[0])
         ctx.sync()
         dt = time.perf_counter() - t0
         for th in threads:
@@ -75,10 +80,12 @@ def main():
         return {"seconds": round(dt, 3), "train_samples_per_s": round(a.steps * B / dt, 1),
                 "validations": len(mses), "val_mse_last": mses[-1] if mses else None}
 
-    inline = run(False)
-    offl = run(True)
-    print(json.dumps({"steps": a.steps, "every": a.every, "inline": inline, "offloaded": offl,
-                      "speedup": round(inline["seconds"] / offl["seconds"], 3)}))
+    for dev_fields in (False, True):
+        inline = run(False, dev_fields)
+        offl = run(True, dev_fields)
+        print(json.dumps({"steps": a.steps, "every": a.every, "heldout_fields": "device" if dev_fields else "host",
+                          "inline": inline, "offloaded": offl,
+                          "speedup": round(inline["seconds"] / offl["seconds"], 3)}), flush=True)
 
 
 if __name__ == "__main__":
