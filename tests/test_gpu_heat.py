@@ -20,7 +20,7 @@ def _ulps(a, b):
     return np.abs(a - b)                      # fields are positive kelvin: ordered bit patterns
 
 
-@pytest.mark.parametrize("n,tau", [(3, 3), (12, 6), (41, 10), (100, 5)])
+@pytest.mark.parametrize("n,tau", [(3, 3), (5, 1), (12, 6), (41, 10), (100, 5)])
 def test_fields_match_the_scheme(n, tau):
     gen = mel.Heat(n, tau)
     assert gen.basis_bytes == 5 * tau * n * n * 8

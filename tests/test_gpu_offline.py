@@ -70,3 +70,18 @@ def test_offline_epochs_follow_the_oracle(tmp_path, precision):
     if precision == mel.FP32:
         assert max(rel_norm(a, b) for a, b in zip(tensors_f64(after["p"]), p)) <= 1e-5
     ds.close()
+
+
+def test_offline_dataset_smaller_than_a_batch(tmp_path):
+    """count < B: no full batch in an epoch (the partial tail is dropped, R24) -> 0 steps."""
+    n, B = 100, 16
+    recs = _records(1, 10, n)
+    path = str(tmp_path / "small.bin")
+    mel.write_dataset(path, n, recs)
+    ds = mel.Dataset(path, threads=2)
+    ctx = mel.Context(mel.Config(n_field=n, hidden=(32,), capacity=2 * B, threshold=0, batch=B, steps_per_sim=10,
+                                 staging_entries=2 * B, policy=mel.FIFO))
+    steps, losses = ctx.train_offline(ds, seed=1, epoch=0)
+    assert steps == 0 and len(losses) == 0
+    assert ctx.get_state()["k"] == 0
+    ds.close()

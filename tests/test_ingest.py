@@ -155,3 +155,19 @@ def test_full_ring_and_protocol_errors(lib):
         mel.Client("no_such_ring_" + name, 1, 0)
     cl.close()
     ing.destroy()
+
+
+def test_clients_that_only_finalize_reach_eos(lib):
+    """Clients that connect and finalize without sending (an empty simulation) still count
+    toward EOS; nothing is returned."""
+    n, name = 16, _name()
+    ing = mel.Ingest(name, 0, n, slots=4, expected_clients=2)
+    for c in (4, 9):
+        cl = mel.Client(name, 1, c)
+        assert cl.finalize() == mel.OK
+        cl.close()
+    st, m = ing.next(1000)
+    assert st == mel.EOS and m is None
+    s = ing.stats()
+    assert s["finalized"] == 2 and s["received"] == 0
+    ing.destroy()
