@@ -294,7 +294,6 @@ int reservoir_stats(mel_ctx* ctx, mel_stats* out);
 int reservoir_dump(mel_ctx* ctx, uint32_t* sim_host, uint32_t* t_host, float* X_host /*C x 5*/,
                    uint32_t* seen_host, uint64_t* put_seq_host, void* payload_host);
 
-/* Waits for all work queued on the context's stream. */
 /* Validation on a dedicated GPU (validation stalls the consumer):
  * copies src's fp32 parameters (every layer; W_L gathered under ZeRO, collectively) into
  * dst, a context of the same layout on another GPU, over NVLink (cudaMemcpyPeerAsync), and
@@ -303,6 +302,8 @@ int reservoir_dump(mel_ctx* ctx, uint32_t* sim_host, uint32_t* t_host, float* X_
  * dst runs beside src's training.  MEL_EINVAL if the layouts differ.  The Adam moments and
  * step counters are not copied. */
 int mel_params_copy(mel_ctx* dst, mel_ctx* src);
+
+/* Waits for all work queued on the context's stream. */
 int mel_sync(mel_ctx* ctx);
 
 /* Per-kernel timing (flag MEL_FLAG_TIMING): total milliseconds and launch count

@@ -7,7 +7,7 @@
  * §3.2.2 "Data distribution"):
  *   - clients are separate processes; "A first call is required to connect the client to
  *     the server (init_communication). A send is issued to transfer time steps u_X^t as
- *     soon as computed. Eventually, a client calls finialize_communication" (P:189);
+ *     soon as computed. Eventually, a client calls finialize_communication" (P:187);
  *   - "they are gathered and then converted, typically from 64 to 32 bits" -- on the
  *     client, so the server is not loaded with the conversion;
  *   - "each client connects to all the ranks of the server and distributes the produced
@@ -108,7 +108,7 @@ int mel_ingest_segment(const mel_ingest* ing, void** base, uint64_t* bytes);
 /* Unmaps and unlinks the segment. */
 void mel_ingest_destroy(mel_ingest* ing);
 
-/* ---- client side (P:189) ------------------------------------------------------------ */
+/* ---- client side (P:187) ------------------------------------------------------------ */
 
 /* init_communication: maps the rings "/<name>.0" ... "/<name>.<world-1>" (they must
  * exist).  MEL_EPROTO if a ring has another layout, MEL_ENOMEM if one is missing. */

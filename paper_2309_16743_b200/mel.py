@@ -505,7 +505,7 @@ class Ingest:
 
 
 class Client:
-    """A simulation client (P:189): init_communication / send / finalize_communication."""
+    """A simulation client (P:187): init_communication / send / finalize_communication."""
 
     def __init__(self, name: str, world: int, client_id: int, lib=None):
         self.lib = lib or load_ingest_library()
