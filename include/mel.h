@@ -264,8 +264,11 @@ int reservoir_sample_batch(mel_ctx* ctx, int32_t* slots_host, uint32_t* n_host);
  * COLLECTIVE when world > 1: every rank calls it the same number of times; a rank
  * without a batch contributes 0 samples.  loss_host (nullable): global mean loss
  * of this step (synchronises); NULL keeps the step asynchronous.
- * Returns MEL_OK, MEL_EAGAIN (no rank had samples: nothing done), MEL_EOS (every
- * rank closed and drained), MEL_ENONFINITE (loss not finite), errors. */
+ * Returns MEL_OK, MEL_EAGAIN (no rank had samples: nothing done -- the parameters,
+ * moments and step counters are unchanged; at world 1 the call launches no training
+ * kernel at all, only the record of its status for surrogate_step_result, and
+ * synchronises), MEL_EOS (every rank closed and drained), MEL_ENONFINITE (loss not
+ * finite), errors. */
 int surrogate_step(mel_ctx* ctx, double* loss_host);
 
 /* Result of an earlier surrogate_step call without draining the stream: `call` is the

@@ -14,8 +14,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
-OUT = os.path.join(HERE, "libmel.so")
-OBJ = os.path.join(HERE, "build_obj")
+OUT = os.path.join(HERE, os.environ.get("MEL_BUILD_NAME", "libmel.so"))   # variant builds (A/B timing)
+OBJ = os.path.join(HERE, "build_obj" + os.environ.get("MEL_BUILD_NAME", ""))
 SOURCES = ["mel.cu", "reservoir.cu", "mlp_simt.cu", "tc_out.cu", "ingest.cpp", "dataset.cpp", "heat.cu"]
 INGEST_OUT = os.path.join(HERE, "libmel_ingest.so")   # host-only, for the simulation clients
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -46,6 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", inc,
                     "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+    flags += os.environ.get("MEL_NVCC_DEFS", "").split()       # -D overrides of tuning macros (A/B builds)
 
     def compile_one(src):
         obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")

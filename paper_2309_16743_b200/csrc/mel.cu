@@ -134,6 +134,7 @@ struct mel_ctx {
   uint32_t* p_cnt[tc::MAX_WORLD] = {};
   __nv_bfloat16* p_sh[2][tc::MAX_WORLD] = {};
   uint32_t epoch = 0;
+  uint32_t k1_launches = 0;                 // tags the overlapped K1's hand-off queue entries
 
   // timing
   std::vector<TimedPair> pending;
@@ -504,6 +505,7 @@ int train_step_bf16(mel_ctx* c) {
     a.adam_p = c->d_p + offW; a.adam_m = c->d_m + offW; a.adam_v = c->d_v + offW;
     a.shadow_out = c->d_shadow[c->shadow_cur ^ 1];
     a.sd = c->d_sd;
+    a.k1_seq = c->k1_launches++;
     a.b1 = (float)c->cfg.beta1; a.b2 = (float)c->cfg.beta2; a.eps = (float)c->cfg.eps;
     if (c->peer) {
       // the Adam inside K1 needs the global batch size (gradient scale, skip) up front
@@ -1295,6 +1297,25 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
     c->batch_n = 0;
   }
   int r;
+  if (c->world == 1 && c->batch_n == 0) {
+    // no samples (watermark gate, drained, or no sample call): nothing to train on, so no
+    // gather / forward / backward / Adam is launched and the parameters and the shadow stay
+    // as they are; only the step's result (status 1, as step_finalize publishes it for an
+    // empty step) is recorded in stream order for surrogate_step_result
+    CK(cudaMemsetAsync(c->d_sd->red, 0, sizeof c->d_sd->red, c->stream));
+    {
+      Timer t(c, MEL_K_LOSS, 1);
+      step_finalize(c->d_sd, (double)c->N, c->cfg.lr0, c->cfg.lr_min, c->cfg.lr_halving_samples, c->cfg.beta1,
+                    c->cfg.beta2, c->d_mirror, c->d_st, c->stream, (uint32_t)(c->calls % MEL_RESULT_RING));
+    }
+    if ((r = check_launch(c, "empty step"))) return r;
+    CK(cudaEventRecord(c->ev_call[c->calls % MEL_RESULT_RING], c->stream));
+    c->calls += 1;
+    c->batch_known = false;
+    if ((r = sync_stream(c))) return r;
+    const Mirror& m = *c->h_mirror;
+    return (c->closed && m.over && m.p == 0) ? MEL_EOS : MEL_EAGAIN;
+  }
   {
     Timer t(c, MEL_K_GATHER, 1);
     launch_gather(c->ra, c->d_slots, c->B, c->cfg.steps_per_sim, c->d_xn, c->stream);

@@ -13,6 +13,9 @@ namespace tc {
 struct TcBuffers {
   __nv_bfloat16* h_bf16 = nullptr;   // [B][K] last hidden activations (bf16)
   __nv_bfloat16* dyT = nullptr;      // [Npad][B] dS/dY transposed (bf16)
+  float* ring = nullptr;             // overlapped K1: per-CTA dW hand-off ring [160][2][128][K] fp32
+  void* ctl = nullptr;               // overlapped K1: queue / ring counters (tc_out.cu K1Ctl)
+  void* entries = nullptr;           // overlapped K1: queue of handed-off tiles [Npad / 128]
   void* maps = nullptr;              // device copy of the TMA descriptors
   void* h_maps = nullptr;            // host copies (CUtensorMap)
   uint64_t Npad = 0;
@@ -50,6 +53,7 @@ struct OutTcArgs {
   float *adam_p, *adam_m, *adam_v;   // W_L fp32 master / moments (fused)
   __nv_bfloat16* shadow_out;         // updated bf16 shadow (fused), the other buffer
   const StepDev* sd;                 // step scalars (scale, lr, bias corrections, skip)
+  uint32_t k1_seq;                   // launch counter (tags the overlapped K1's queue entries)
   float b1, b2, eps;
   // in-kernel exchange (world > 1, bf16; tc_out.cu K1Params): the fused Adam runs on the
   // tiles this rank owns, the other tiles' dW are reduce-added into their owners' acc
