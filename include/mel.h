@@ -309,6 +309,26 @@ int mel_params_copy(mel_ctx* dst, mel_ctx* src);
 /* Waits for all work queued on the context's stream. */
 int mel_sync(mel_ctx* ctx);
 
+/* Virtual ranks (test mode; "the locally computed vector of weight updates is
+ * all-reduced", SURVEY 4.2 T3'): `world` (2..8) ranks on ONE device, so that the
+ * data-parallel path -- in bf16 mode the in-kernel gradient exchange of the output layer
+ * (dW tiles TMA-stored / reduce-added into the owner rank's buffer, owner-side fused Adam,
+ * new shadow rows pushed to every rank) -- runs and is checked on a single GPU.  Creates
+ * `world` contexts (out[world], rank order) on cuda_device sharing `stream` (NULL: one is
+ * created), each a full rank (own reservoir, batch, replica); they are used with every call
+ * above except surrogate_step.  Their collectives run as device-side rank-ordered sums, and
+ * the output layer's K1 as ONE cooperative launch of world x floor(#SMs / world) CTAs over
+ * every rank's tiles (the ranks' CTAs wait on one another, so they must be co-resident).
+ * bf16 mode needs the in-kernel exchange (no MEL_FLAG_NCCL_EXCHANGE / MEL_FLAG_NO_ZERO);
+ * fp32 mode all-reduces the flat gradient.  Release each context with mel_destroy.
+ * MEL_EINVAL, MEL_ENOMEM, MEL_ECUDA (nothing created). */
+int mel_create_virtual(const mel_config* cfg, int world, int cuda_device, void* stream, mel_ctx** out);
+
+/* One collective surrogate_step over the virtual ranks ctxs[0..world) (rank order; each
+ * rank's batch is its last reservoir_sample_batch).  Same semantics and statuses as
+ * surrogate_step at `world` ranks; loss_host (nullable) receives the global loss. */
+int surrogate_step_virtual(mel_ctx* const* ctxs, int world, double* loss_host);
+
 /* Per-kernel timing (flag MEL_FLAG_TIMING): total milliseconds and launch count
  * of kernel class `k` (enum mel_kernel) since the last reset, measured with CUDA
  * events on the launching stream.  Synchronises. */

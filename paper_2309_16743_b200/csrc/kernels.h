@@ -123,6 +123,10 @@ void step_finalize(StepDev* sd, double n_field, double lr0, double lr_min, uint6
 void step_prepare(StepDev* sd, const ResDev* st, double n_field, double lr0, double lr_min, uint64_t halving, double b1,
                   double b2, cudaStream_t s, bool global_n = false);   // global_n: use sd->n_glob
 void stage_count(StepDev* sd, const ResDev* st, cudaStream_t s);     // sd->n_glob = st->n_last
+// virtual ranks: bufs[q][i] <- sum over q of bufs[q][i] (rank order), for every q; d_bufs is a
+// device array of R pointers
+void vsum_f32(float* const* d_bufs, int R, uint64_t n, cudaStream_t s);
+void vsum_f64(double* const* d_bufs, int R, uint64_t n, cudaStream_t s);
 void adam_flat(float* p, float* m, float* v, const float* g, uint64_t n, const StepDev* sd,
                float b1, float b2, float eps, __nv_bfloat16* shadow, uint64_t sh_begin, uint64_t sh_end,
                cudaStream_t s);

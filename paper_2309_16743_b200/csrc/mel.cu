@@ -32,8 +32,24 @@ struct TimedPair {
 
 }  // namespace
 
+// Virtual ranks (mel_create_virtual): R contexts on one device and one stream; the
+// collectives are device-side rank-ordered sums over the members' buffers and K1 runs as one
+// cooperative launch over every member's tiles (tc::launch_out_fwd_dw_virtual).
+struct VGroup {
+  int R = 0, refs = 0;
+  mel_ctx* cs[tc::MAX_WORLD] = {};
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  void* d_desc = nullptr;                  // K1Virt[R]
+  float** d_tab_g = nullptr;               // [R] every member's flat gradient buffer
+  double** d_tab_red = nullptr;            // [R] &d_sd->red[0]
+  double** d_tab_nglob = nullptr;          // [R] &d_sd->n_glob
+};
+
 struct mel_ctx {
   mel_config cfg{};
+  bool virt = false;                        // a member of a virtual-rank group
+  VGroup* vg = nullptr;
   int rank = 0, world = 1, dev = 0;
   cudaStream_t stream = nullptr, copy_stream = nullptr;
   bool own_stream = false;
@@ -382,6 +398,20 @@ int wait_shadow(mel_ctx* c) {
 int gather_master(mel_ctx* c, bool moments) {
   if (!c->zero) return MEL_OK;
   const uint64_t offW = c->off[2 * (c->L - 1)];
+  if (c->peer && c->virt) {
+    // virtual ranks: the rows every other member owns, copied from its buffers
+    const uint64_t offW = c->off[2 * (c->L - 1)];
+    for (int q = 0; q < c->world; ++q) {
+      if (q == c->rank) continue;
+      mel_ctx* o = c->vg->cs[q];
+      tc::copy_owned_rows(c->tcb, o->d_p + offW, c->d_p + offW, c->Klast, q, c->world, c->stream);
+      if (moments) {
+        tc::copy_owned_rows(c->tcb, o->d_m + offW, c->d_m + offW, c->Klast, q, c->world, c->stream);
+        tc::copy_owned_rows(c->tcb, o->d_v + offW, c->d_v + offW, c->Klast, q, c->world, c->stream);
+      }
+    }
+    return check_launch(c, "virtual gather");
+  }
   if (c->peer) {
     // owners are interleaved by tile (tc::tile_owner): every rank contributes its owned
     // rows and zeros elsewhere; an integer sum of the bit patterns is an exact gather.
@@ -492,10 +522,11 @@ int train_step_fp32(mel_ctx* c) {
   return MEL_OK;
 }
 
-int train_step_bf16(mel_ctx* c) {
+// the output layer's kernel arguments (no launches)
+void bf16_args(mel_ctx* c, tc::OutTcArgs& a) {
   const int L = c->L;
   const uint32_t B = c->B, K = c->Klast;
-  tc::OutTcArgs a{};
+  a = tc::OutTcArgs{};
   a.N = c->N; a.Npad = c->Npad; a.B = B; a.K = K;
   a.shadow_idx = c->shadow_cur;
   a.w_bf16 = c->d_shadow[c->shadow_cur];
@@ -507,15 +538,6 @@ int train_step_bf16(mel_ctx* c) {
     a.sd = c->d_sd;
     a.k1_seq = c->k1_launches++;
     a.b1 = (float)c->cfg.beta1; a.b2 = (float)c->cfg.beta2; a.eps = (float)c->cfg.eps;
-    if (c->peer) {
-      // the Adam inside K1 needs the global batch size (gradient scale, skip) up front
-      Timer t(c, MEL_K_ALLREDUCE, 1);
-      stage_count(c->d_sd, c->d_st, c->stream);
-      NK(ncclAllReduce(&c->d_sd->n_glob, &c->d_sd->n_glob, 1, ncclFloat64, ncclSum, c->comm, c->stream));
-    }
-    Timer t(c, MEL_K_LOSS, 1);
-    step_prepare(c->d_sd, c->d_st, (double)c->N, c->cfg.lr0, c->cfg.lr_min, c->cfg.lr_halving_samples,
-                 c->cfg.beta1, c->cfg.beta2, c->stream, c->peer);
   }
   if (c->peer) {
     a.peer = 1; a.rank = (uint32_t)c->rank; a.world = (uint32_t)c->world; a.epoch = ++c->epoch;
@@ -534,6 +556,41 @@ int train_step_bf16(mel_ctx* c) {
   a.dh_part = c->d_part;
   a.dz = c->d_dz[L - 2];
   a.z = c->d_z[L - 2];
+}
+
+// step scalars ahead of K1 (the fused Adam needs lr, bias corrections, the gradient scale)
+void bf16_prepare(mel_ctx* c) {
+  Timer t(c, MEL_K_LOSS, 1);
+  step_prepare(c->d_sd, c->d_st, (double)c->N, c->cfg.lr0, c->cfg.lr_min, c->cfg.lr_halving_samples,
+               c->cfg.beta1, c->cfg.beta2, c->stream, c->peer);
+}
+
+// after K1: K2 (dH) and this rank's SSE
+int bf16_post_k1(mel_ctx* c, const tc::OutTcArgs& a, int nparts) {
+  {
+    Timer t(c, MEL_K_OUT_DH, 2);
+    tc::launch_out_dh(a, c->tcb, c->stream);
+  }
+  int r = check_launch(c, "output layer tcgen05");
+  if (r) return r;
+  reduce_local(c->d_sd, c->d_sse_part, nparts, c->d_st, c->stream);
+  return MEL_OK;
+}
+
+int train_step_bf16(mel_ctx* c) {
+  const int L = c->L;
+  const uint32_t K = c->Klast;
+  tc::OutTcArgs a;
+  bf16_args(c, a);
+  if (a.fused_adam) {
+    if (c->peer) {
+      // the Adam inside K1 needs the global batch size (gradient scale, skip) up front
+      Timer t(c, MEL_K_ALLREDUCE, 1);
+      stage_count(c->d_sd, c->d_st, c->stream);
+      NK(ncclAllReduce(&c->d_sd->n_glob, &c->d_sd->n_glob, 1, ncclFloat64, ncclSum, c->comm, c->stream));
+    }
+    bf16_prepare(c);
+  }
   int nparts = 0;
   if (!c->zero || c->peer) {
     int r0 = wait_shadow(c);
@@ -557,13 +614,86 @@ int train_step_bf16(mel_ctx* c) {
     }
     c->ag_pending = false;
   }
-  {
-    Timer t(c, MEL_K_OUT_DH, 2);
-    tc::launch_out_dh(a, c->tcb, c->stream);
+  return bf16_post_k1(c, a, nparts);
+}
+
+// a step's front: the batch bookkeeping, the gather of the batch inputs, the head forward
+int step_front(mel_ctx* c) {
+  if (!c->batch_known) {
+    // no sample since the last step: this rank contributes nothing
+    CK(cudaMemsetAsync(&c->d_st->n_last, 0, 4, c->stream));
+    c->batch_n = 0;
   }
-  int r = check_launch(c, "output layer tcgen05");
-  if (r) return r;
-  reduce_local(c->d_sd, c->d_sse_part, nparts, c->d_st, c->stream);
+  {
+    Timer t(c, MEL_K_GATHER, 1);
+    launch_gather(c->ra, c->d_slots, c->B, c->cfg.steps_per_sim, c->d_xn, c->stream);
+  }
+  {
+    Timer t(c, MEL_K_HEAD_FWD, 0);
+    const int nl = head_forward(c, c->d_xn, c->d_z, c->d_h, (int)c->B,
+                                c->cfg.precision == MEL_BF16 ? c->tcb.h_bf16 : nullptr);
+    c->launches += nl;
+    c->klaunch[MEL_K_HEAD_FWD] += nl;
+  }
+  return check_launch(c, "head forward");
+}
+
+// a step's end, after the gradient exchange: loss / step scalars, Adam (the part K1 did not
+// fuse), the shadow flip, the result record for surrogate_step_result
+int step_finish(mel_ctx* c) {
+  int r;
+  {
+    Timer t(c, MEL_K_LOSS, 1);
+    step_finalize(c->d_sd, (double)c->N, c->cfg.lr0, c->cfg.lr_min, c->cfg.lr_halving_samples, c->cfg.beta1,
+                  c->cfg.beta2, c->d_mirror, c->d_st, c->stream, (uint32_t)(c->calls % MEL_RESULT_RING));
+  }
+  if (c->fused_adam || c->peer) {
+    // W_L was updated inside K1 (new shadow in the other buffer, written to every rank in
+    // exchange mode); the small region here
+    Timer t(c, MEL_K_ADAM, 1);
+    adam_flat(c->d_p, c->d_m, c->d_v, c->d_g, c->off[2 * (c->L - 1)], c->d_sd, (float)c->cfg.beta1,
+              (float)c->cfg.beta2, (float)c->cfg.eps, nullptr, 0, 0, c->stream);
+    c->shadow_cur ^= 1;
+  } else if (c->zero) {
+    // small region (head weights, every bias) replicated; W_L on this rank's row shard,
+    // refreshing the shard of the bf16 shadow, then all-gather of the shadow
+    Timer t(c, MEL_K_ADAM, 1 + c->nb);
+    const uint64_t offW = c->off[2 * (c->L - 1)];
+    const float b1 = (float)c->cfg.beta1, b2 = (float)c->cfg.beta2, eps = (float)c->cfg.eps;
+    adam_flat(c->d_p, c->d_m, c->d_v, c->d_g, offW, c->d_sd, b1, b2, eps, nullptr, 0, 0, c->stream);
+    for (int j = 0; j < c->nb; ++j) {
+      const uint64_t po = part_off(c, j), so = offW + po, n = part_elems(c, j);
+      adam_flat(c->d_p + so, c->d_m + so, c->d_v + so, c->d_g + so, n, c->d_sd, b1, b2, eps,
+                c->d_shadow[c->shadow_cur] + po, 0, n, c->stream);
+    }
+  } else {
+    Timer t(c, MEL_K_ADAM, 1);
+    __nv_bfloat16* sh = nullptr;
+    uint64_t b0 = 0, b1 = 0;
+    if (c->cfg.precision == MEL_BF16) {
+      // the output-layer kernels of this step have completed (stream order), so
+      // the bf16 shadow is refreshed in place from the updated fp32 master
+      sh = c->d_shadow[c->shadow_cur];
+      b0 = c->off[2 * (c->L - 1)];
+      b1 = b0 + c->Npad * c->Klast;
+    }
+    adam_flat(c->d_p, c->d_m, c->d_v, c->d_g, c->n_flat, c->d_sd, (float)c->cfg.beta1, (float)c->cfg.beta2,
+              (float)c->cfg.eps, sh, b0, b1, c->stream);
+  }
+  if (c->zero && !c->peer) {
+    Timer t(c, MEL_K_ALLREDUCE, 0, c->comm_stream);
+    CK(cudaEventRecord(c->ev_adam, c->stream));
+    CK(cudaStreamWaitEvent(c->comm_stream, c->ev_adam, 0));
+    for (int j = 0; j < c->nb; ++j) {
+      if ((r = gather_bucket(c, c->d_shadow[c->shadow_cur], 2, ncclBfloat16, j))) return r;
+      CK(cudaEventRecord(c->ev_agb[j], c->comm_stream));
+    }
+    c->ag_pending = true;
+  }
+  if ((r = check_launch(c, "adam"))) return r;
+  CK(cudaEventRecord(c->ev_call[c->calls % MEL_RESULT_RING], c->stream));
+  c->calls += 1;
+  c->batch_known = false;
   return MEL_OK;
 }
 
@@ -664,7 +794,8 @@ static int setup_peer(mel_ctx* c) {
 static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, void* stream) {
   int r = validate(g, c->world, c);
   if (r) return r;
-  if ((c->world > 1) != (nccl_id != nullptr)) return fail(c, MEL_EINVAL, "nccl_id must be given iff world > 1");
+  if (!c->virt && (c->world > 1) != (nccl_id != nullptr))
+    return fail(c, MEL_EINVAL, "nccl_id must be given iff world > 1");
   c->cfg = *g;
   CK(cudaSetDevice(c->dev));
   if (stream) { c->stream = (cudaStream_t)stream; }
@@ -816,11 +947,13 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
 
   c->fused_adam = (c->world == 1) && (g->precision == MEL_BF16) && !(g->flags & MEL_FLAG_UNFUSED_ADAM);
   if (c->world > 1) {
-    ncclUniqueId id;
-    memcpy(&id, nccl_id, sizeof id);
-    ncclConfig_t ncfg = NCCL_CONFIG_INITIALIZER;
-    if (c->zero && c->sm_reserve > 0) ncfg.maxCTAs = c->sm_reserve;   // NCCL on the SMs the kernels leave free
-    NK(ncclCommInitRankConfig(&c->comm, c->world, id, c->rank, &ncfg));
+    if (!c->virt) {
+      ncclUniqueId id;
+      memcpy(&id, nccl_id, sizeof id);
+      ncclConfig_t ncfg = NCCL_CONFIG_INITIALIZER;
+      if (c->zero && c->sm_reserve > 0) ncfg.maxCTAs = c->sm_reserve;   // NCCL on the SMs the kernels leave free
+      NK(ncclCommInitRankConfig(&c->comm, c->world, id, c->rank, &ncfg));
+    }
     c->shard_elems = c->Npad / c->world * c->Klast;
     c->shard_off = (uint64_t)c->rank * c->shard_elems;
     CK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
@@ -830,7 +963,7 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
       CK(cudaEventCreateWithFlags(&c->ev_k1[j], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_agb[j], cudaEventDisableTiming));
     }
-    if (c->zero && !(g->flags & MEL_FLAG_NCCL_EXCHANGE) && c->world <= tc::MAX_WORLD) {
+    if (!c->virt && c->zero && !(g->flags & MEL_FLAG_NCCL_EXCHANGE) && c->world <= tc::MAX_WORLD) {
       r = setup_peer(c);
       if (r) return r;
     }
@@ -869,7 +1002,7 @@ void mel_destroy(mel_ctx* c) {
   }
   if (c->ing_pinned) cudaHostUnregister(c->ing_base);
   if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
-  if (c->peer) {
+  if (c->peer && !c->virt) {
     for (int q = 0; q < c->world; ++q) {
       if (q == c->rank) continue;
       void* h[] = {c->p_acc[q], c->p_cnt[q], c->p_sh[0][q], c->p_sh[1][q]};
@@ -907,7 +1040,111 @@ void mel_destroy(mel_ctx* c) {
     if (c->ev_call[i]) cudaEventDestroy(c->ev_call[i]);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  if (c->vg) {
+    VGroup* vg = c->vg;
+    vg->cs[c->rank] = nullptr;
+    if (--vg->refs == 0) {
+      void* ptrs[] = {vg->d_desc, vg->d_tab_g, vg->d_tab_red, vg->d_tab_nglob};
+      for (void* p : ptrs)
+        if (p) cudaFree(p);
+      if (vg->own_stream && vg->stream) cudaStreamDestroy(vg->stream);
+      delete vg;
+    }
+  }
   delete c;
+}
+
+// Virtual ranks (test mode): `world` contexts on ONE device sharing one stream, each a full
+// rank (its own reservoir, batch and replica); their collectives run as device-side
+// rank-ordered sums and the bf16 in-kernel exchange as one cooperative K1 launch over every
+// rank's tiles, ~#SMs / world CTAs per rank.  out[world] receives the contexts in rank order.
+int mel_create_virtual(const mel_config* g, int world, int cuda_device, void* stream, mel_ctx** out) {
+  if (!g || !out || world < 2 || world > tc::MAX_WORLD) return MEL_EINVAL;
+  for (int q = 0; q < world; ++q) out[q] = nullptr;
+  if (g->precision == MEL_BF16 && (g->flags & (MEL_FLAG_NCCL_EXCHANGE | MEL_FLAG_NO_ZERO))) {
+    fprintf(stderr, "mel_create_virtual: bf16 virtual ranks run the in-kernel exchange only\n");
+    return MEL_EINVAL;
+  }
+  if (cudaSetDevice(cuda_device) != cudaSuccess) return MEL_ECUDA;
+  VGroup* vg = new VGroup();
+  vg->R = world;
+  if (stream) {
+    vg->stream = (cudaStream_t)stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&vg->stream, cudaStreamNonBlocking) != cudaSuccess) { delete vg; return MEL_ECUDA; }
+    vg->own_stream = true;
+  }
+  int r = MEL_OK;
+  auto cleanup = [&]() {
+    for (int q = 0; q < world; ++q)
+      if (out[q]) { mel_destroy(out[q]); out[q] = nullptr; }
+  };
+  for (int q = 0; q < world; ++q) {
+    mel_ctx* c = new mel_ctx();
+    c->rank = q; c->world = world; c->dev = cuda_device; c->virt = true; c->vg = vg;
+    vg->cs[q] = c;
+    vg->refs += 1;
+    out[q] = c;
+    r = create_impl(c, g, nullptr, vg->stream);
+    if (r) {
+      fprintf(stderr, "mel_create_virtual (rank %d): %s\n", q, c->err.c_str());
+      cleanup();
+      return r;
+    }
+  }
+  mel_ctx* c = out[0];
+  auto alloc_tab = [&](void** dst, const void* const* host) -> int {
+    if (cudaMalloc(dst, sizeof(void*) * world) != cudaSuccess) return MEL_ENOMEM;
+    if (cudaMemcpy(*dst, host, sizeof(void*) * world, cudaMemcpyHostToDevice) != cudaSuccess) return MEL_ECUDA;
+    return MEL_OK;
+  };
+  const void* tg[tc::MAX_WORLD];
+  const void* tr[tc::MAX_WORLD];
+  const void* tn[tc::MAX_WORLD];
+  for (int q = 0; q < world; ++q) {
+    tg[q] = out[q]->d_g; tr[q] = &out[q]->d_sd->red[0]; tn[q] = &out[q]->d_sd->n_glob;
+  }
+  if ((r = alloc_tab((void**)&vg->d_tab_g, tg)) || (r = alloc_tab((void**)&vg->d_tab_red, tr)) ||
+      (r = alloc_tab((void**)&vg->d_tab_nglob, tn))) {
+    cleanup();
+    return r;
+  }
+  if (g->precision == MEL_BF16) {
+    // the in-kernel exchange between the members: every member's acc, counters and shadows
+    // addressed directly (one device), K1 grid = #SMs / world CTAs per rank
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
+    const int G = sms / world;
+    if (cudaMalloc(&vg->d_desc, (size_t)tc::virt_desc_bytes() * world) != cudaSuccess) { cleanup(); return MEL_ENOMEM; }
+    for (int q = 0; q < world; ++q) {
+      mel_ctx* m = out[q];
+      m->tcb.fwd_ctas = G < 160 ? G : 160;
+      m->acc_bf16 = !(g->flags & MEL_FLAG_FP32_EXCHANGE) && m->Klast % 128 == 0;
+      const size_t acc_bytes = (m->acc_bf16 ? 2 : 4) * m->Npad * m->Klast;
+      if (cudaMalloc(&m->d_acc, acc_bytes) != cudaSuccess || cudaMemset(m->d_acc, 0, acc_bytes) != cudaSuccess ||
+          cudaMalloc(&m->d_cnt, 4 * (m->Npad / 128)) != cudaSuccess ||
+          cudaMemset(m->d_cnt, 0, 4 * (m->Npad / 128)) != cudaSuccess) {
+        cleanup();
+        return MEL_ENOMEM;
+      }
+    }
+    for (int q = 0; q < world; ++q) {
+      mel_ctx* m = out[q];
+      for (int p = 0; p < world; ++p) {
+        m->p_acc[p] = out[p]->d_acc; m->p_cnt[p] = out[p]->d_cnt;
+        m->p_sh[0][p] = out[p]->d_shadow[0]; m->p_sh[1][p] = out[p]->d_shadow[1];
+      }
+      if (tc::prepare_peer(m->tcb, m->Klast, m->Npad, m->rank, world, m->p_acc, m->acc_bf16, m->p_sh[0], m->p_sh[1])) {
+        fprintf(stderr, "mel_create_virtual: exchange tensor maps: %s\n", tc::last_error());
+        cleanup();
+        return MEL_ECUDA;
+      }
+      m->peer = true;
+    }
+  }
+  if (cudaStreamSynchronize(vg->stream) != cudaSuccess) { cleanup(); return MEL_ECUDA; }
+  (void)c;
+  return MEL_OK;
 }
 
 int mel_param_layout(const mel_ctx* c, uint32_t* n_tensors, uint32_t* shapes, uint64_t* total) {
@@ -1290,18 +1527,16 @@ int reservoir_sample_batch(mel_ctx* c, int32_t* slots_host, uint32_t* n_host) {
 
 int surrogate_step(mel_ctx* c, double* loss_host) {
   GUARD(c);
+  if (c->virt) return fail(c, MEL_EPROTO, "a virtual rank steps through surrogate_step_virtual");
   const bool local_has = c->batch_known && c->batch_n > 0;
-  if (!c->batch_known) {
-    // no sample since the last step: this rank contributes nothing
-    CK(cudaMemsetAsync(&c->d_st->n_last, 0, 4, c->stream));
-    c->batch_n = 0;
-  }
+  if (!c->batch_known) c->batch_n = 0;
   int r;
   if (c->world == 1 && c->batch_n == 0) {
     // no samples (watermark gate, drained, or no sample call): nothing to train on, so no
     // gather / forward / backward / Adam is launched and the parameters and the shadow stay
     // as they are; only the step's result (status 1, as step_finalize publishes it for an
     // empty step) is recorded in stream order for surrogate_step_result
+    CK(cudaMemsetAsync(&c->d_st->n_last, 0, 4, c->stream));
     CK(cudaMemsetAsync(c->d_sd->red, 0, sizeof c->d_sd->red, c->stream));
     {
       Timer t(c, MEL_K_LOSS, 1);
@@ -1316,74 +1551,12 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
     const Mirror& m = *c->h_mirror;
     return (c->closed && m.over && m.p == 0) ? MEL_EOS : MEL_EAGAIN;
   }
-  {
-    Timer t(c, MEL_K_GATHER, 1);
-    launch_gather(c->ra, c->d_slots, c->B, c->cfg.steps_per_sim, c->d_xn, c->stream);
-  }
-  {
-    Timer t(c, MEL_K_HEAD_FWD, 0);
-    const int nl = head_forward(c, c->d_xn, c->d_z, c->d_h, (int)c->B,
-                                c->cfg.precision == MEL_BF16 ? c->tcb.h_bf16 : nullptr);
-    c->launches += nl;
-    c->klaunch[MEL_K_HEAD_FWD] += nl;
-  }
-  if ((r = check_launch(c, "head forward"))) return r;
+  if ((r = step_front(c))) return r;
   r = c->cfg.precision == MEL_FP32 ? train_step_fp32(c) : train_step_bf16(c);
   if (r) return r;
   if ((r = head_backward(c))) return r;
   if ((r = world_exchange(c))) return r;
-  {
-    Timer t(c, MEL_K_LOSS, 1);
-    step_finalize(c->d_sd, (double)c->N, c->cfg.lr0, c->cfg.lr_min, c->cfg.lr_halving_samples, c->cfg.beta1,
-                  c->cfg.beta2, c->d_mirror, c->d_st, c->stream, (uint32_t)(c->calls % MEL_RESULT_RING));
-  }
-  if (c->fused_adam || c->peer) {
-    // W_L was updated inside K1 (new shadow in the other buffer, written to every rank in
-    // exchange mode); the small region here
-    Timer t(c, MEL_K_ADAM, 1);
-    adam_flat(c->d_p, c->d_m, c->d_v, c->d_g, c->off[2 * (c->L - 1)], c->d_sd, (float)c->cfg.beta1,
-              (float)c->cfg.beta2, (float)c->cfg.eps, nullptr, 0, 0, c->stream);
-    c->shadow_cur ^= 1;
-  } else if (c->zero) {
-    // small region (head weights, every bias) replicated; W_L on this rank's row shard,
-    // refreshing the shard of the bf16 shadow, then all-gather of the shadow
-    Timer t(c, MEL_K_ADAM, 1 + c->nb);
-    const uint64_t offW = c->off[2 * (c->L - 1)];
-    const float b1 = (float)c->cfg.beta1, b2 = (float)c->cfg.beta2, eps = (float)c->cfg.eps;
-    adam_flat(c->d_p, c->d_m, c->d_v, c->d_g, offW, c->d_sd, b1, b2, eps, nullptr, 0, 0, c->stream);
-    for (int j = 0; j < c->nb; ++j) {
-      const uint64_t po = part_off(c, j), so = offW + po, n = part_elems(c, j);
-      adam_flat(c->d_p + so, c->d_m + so, c->d_v + so, c->d_g + so, n, c->d_sd, b1, b2, eps,
-                c->d_shadow[c->shadow_cur] + po, 0, n, c->stream);
-    }
-  } else {
-    Timer t(c, MEL_K_ADAM, 1);
-    __nv_bfloat16* sh = nullptr;
-    uint64_t b0 = 0, b1 = 0;
-    if (c->cfg.precision == MEL_BF16) {
-      // the output-layer kernels of this step have completed (stream order), so
-      // the bf16 shadow is refreshed in place from the updated fp32 master
-      sh = c->d_shadow[c->shadow_cur];
-      b0 = c->off[2 * (c->L - 1)];
-      b1 = b0 + c->Npad * c->Klast;
-    }
-    adam_flat(c->d_p, c->d_m, c->d_v, c->d_g, c->n_flat, c->d_sd, (float)c->cfg.beta1, (float)c->cfg.beta2,
-              (float)c->cfg.eps, sh, b0, b1, c->stream);
-  }
-  if (c->zero && !c->peer) {
-    Timer t(c, MEL_K_ALLREDUCE, 0, c->comm_stream);
-    CK(cudaEventRecord(c->ev_adam, c->stream));
-    CK(cudaStreamWaitEvent(c->comm_stream, c->ev_adam, 0));
-    for (int j = 0; j < c->nb; ++j) {
-      if ((r = gather_bucket(c, c->d_shadow[c->shadow_cur], 2, ncclBfloat16, j))) return r;
-      CK(cudaEventRecord(c->ev_agb[j], c->comm_stream));
-    }
-    c->ag_pending = true;
-  }
-  if ((r = check_launch(c, "adam"))) return r;
-  CK(cudaEventRecord(c->ev_call[c->calls % MEL_RESULT_RING], c->stream));
-  c->calls += 1;
-  c->batch_known = false;
+  if ((r = step_finish(c))) return r;
   const bool need_sync = loss_host || !local_has || c->closed;
   if (!need_sync) return MEL_OK;
   if ((r = sync_stream(c))) return r;
@@ -1402,6 +1575,80 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
       CK(cudaStreamSynchronize(c->stream));
       cudaFree(dv);
       eos = v == 1;
+    }
+    return eos ? MEL_EOS : MEL_EAGAIN;
+  }
+  if (loss_host) *loss_host = m.loss;
+  if (!std::isfinite(m.loss)) return fail(c, MEL_ENONFINITE, "loss is not finite (%g)", m.loss);
+  return MEL_OK;
+}
+
+// One collective step of a virtual-rank group (mel_create_virtual), ranks in order: the
+// same per-rank kernels as surrogate_step, the NCCL all-reduces replaced by rank-ordered
+// device sums (vsum_*) and K1 launched once over every rank's tiles.
+int surrogate_step_virtual(mel_ctx* const* cs, int world, double* loss_host) {
+  if (!cs || world < 2 || world > tc::MAX_WORLD) return MEL_EINVAL;
+  VGroup* vg = cs[0] ? cs[0]->vg : nullptr;
+  if (!vg || vg->R != world) return MEL_EINVAL;
+  for (int q = 0; q < world; ++q) {
+    if (!cs[q] || cs[q]->vg != vg || cs[q]->rank != q) return MEL_EINVAL;
+    if (cs[q]->poisoned) return cs[q]->poisoned;
+  }
+  mel_ctx* c = cs[0];
+  cudaSetDevice(c->dev);
+  cudaStream_t s = c->stream;
+  bool any_local = false, closed = false;
+  int r;
+  for (int q = 0; q < world; ++q) {
+    any_local = any_local || (cs[q]->batch_known && cs[q]->batch_n > 0);
+    closed = closed || cs[q]->closed;
+    if ((r = step_front(cs[q]))) return r;
+  }
+  if (c->cfg.precision == MEL_FP32) {
+    for (int q = 0; q < world; ++q)
+      if ((r = train_step_fp32(cs[q]))) return r;
+  } else {
+    tc::OutTcArgs a[tc::MAX_WORLD];
+    const tc::TcBuffers* tb[tc::MAX_WORLD];
+    for (int q = 0; q < world; ++q) {
+      bf16_args(cs[q], a[q]);
+      tb[q] = &cs[q]->tcb;
+      stage_count(cs[q]->d_sd, cs[q]->d_st, s);
+    }
+    vsum_f64(vg->d_tab_nglob, world, 1, s);                       // the global batch size
+    for (int q = 0; q < world; ++q) bf16_prepare(cs[q]);
+    int nparts;
+    {
+      Timer t(c, MEL_K_OUT_FWD_DW, 1);
+      nparts = tc::launch_out_fwd_dw_virtual(a, tb, world, vg->d_desc, s);
+    }
+    if (nparts < 0) return fail(c, MEL_ECUDA, "virtual K1: %s", tc::last_error());
+    for (int q = 0; q < world; ++q)
+      if ((r = bf16_post_k1(cs[q], a[q], nparts))) return r;
+  }
+  for (int q = 0; q < world; ++q)
+    if ((r = head_backward(cs[q]))) return r;
+  {
+    // the gradient exchange: the whole flat gradient (plain mode) or the small region (the
+    // in-kernel exchange reduced W_L inside K1), plus [SSE, n]
+    Timer t(c, MEL_K_ALLREDUCE, 2);
+    const uint64_t n = c->peer ? c->off[2 * (c->L - 1)] : c->n_flat;
+    vsum_f32(vg->d_tab_g, world, n, s);
+    vsum_f64(vg->d_tab_red, world, 2, s);
+  }
+  if ((r = check_launch(c, "virtual exchange"))) return r;
+  for (int q = 0; q < world; ++q)
+    if ((r = step_finish(cs[q]))) return r;
+  const bool need_sync = loss_host || !any_local || closed;
+  if (!need_sync) return MEL_OK;
+  CK(cudaStreamSynchronize(s));
+  for (int q = 0; q < world; ++q) cs[q]->known_consumed = cs[q]->h_mirror->consumed;
+  const Mirror& m = *c->h_mirror;
+  if (m.status == 1) {
+    bool eos = true;
+    for (int q = 0; q < world; ++q) {
+      const Mirror& mq = *cs[q]->h_mirror;
+      eos = eos && cs[q]->closed && mq.over && mq.p == 0;
     }
     return eos ? MEL_EOS : MEL_EAGAIN;
   }

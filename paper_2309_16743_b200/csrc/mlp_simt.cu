@@ -509,3 +509,30 @@ void normalise_fields(const float* src, float* dst, uint64_t n, float lo, float 
 }
 
 }  // namespace mel
+
+namespace mel {
+
+// ---------------------------------------------------------------------------------
+// Virtual ranks (mel_create_virtual): the all-reduce of R ranks living on one device as
+// a rank-ordered sum written back to every rank ("all-reduced"), fp32 or fp64.
+// ---------------------------------------------------------------------------------
+template <typename T>
+__global__ void vsum_kernel(T* const* bufs, int R, uint64_t n) {
+  pdl_enter();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    T acc = bufs[0][i];
+    for (int q = 1; q < R; ++q) acc += bufs[q][i];
+    for (int q = 0; q < R; ++q) bufs[q][i] = acc;
+  }
+}
+
+void vsum_f32(float* const* d_bufs, int R, uint64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  launch_pdl(vsum_kernel<float>, dim3(grid_for(n, 256, 148 * 8)), dim3(256), 0, s, d_bufs, R, n);
+}
+void vsum_f64(double* const* d_bufs, int R, uint64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  launch_pdl(vsum_kernel<double>, dim3(grid_for(n, 256, 148 * 8)), dim3(256), 0, s, d_bufs, R, n);
+}
+
+}  // namespace mel

@@ -84,6 +84,13 @@ int max_sse_parts(uint64_t Npad);
 // forward + MSE gradient + dW_L/db_L (per 128-row tile of W_L); returns #SSE partials
 int launch_out_fwd_dw(const OutTcArgs& a, const TcBuffers& t, cudaStream_t s, uint32_t tile0 = 0, uint32_t tile1 = 0,
                       uint32_t part_base = 0);
+// virtual ranks (mel_create_virtual): ONE cooperative K1 launch over R ranks' tiles, each
+// rank's maps + parameters copied into d_desc (R x virt_desc_bytes() device bytes); returns
+// the per-rank CTA count (= SSE partials per rank)
+int launch_out_fwd_dw_virtual(const OutTcArgs* a, const TcBuffers* const* t, int R, void* d_desc, cudaStream_t s);
+int virt_desc_bytes();
+// dst = src on the rows of the tiles `rank` owns, untouched elsewhere ([Npad][K] fp32)
+void copy_owned_rows(const TcBuffers& t, const float* src, float* dst, uint32_t K, int rank, int world, cudaStream_t s);
 // dS/dH = dY W_L (split-K over N) then the ReLU' mask -> dz
 void launch_out_dh(const OutTcArgs& a, const TcBuffers& t, cudaStream_t s);
 const char* last_error();

@@ -37,7 +37,8 @@ EXPORTS = ["mel_config_default", "mel_nccl_unique_id", "mel_create", "mel_destro
            "surrogate_eval",
            "reservoir_stats", "reservoir_dump", "mel_sync", "mel_kernel_time", "mel_kernel_time_reset",
            "mel_launch_count", "mel_set_flags", "mel_debug_counters", "reservoir_ingest",
-           "surrogate_train_offline", "reservoir_put_generated", "mel_params_copy"]
+           "surrogate_train_offline", "reservoir_put_generated", "mel_params_copy", "mel_create_virtual",
+           "surrogate_step_virtual"]
 # include/mel_heat.h (on-device heat-equation client)
 HEAT_EXPORTS = ["mel_heat_create", "mel_heat_basis_bytes", "mel_heat_grid", "mel_heat_tau", "mel_heat_fields",
                 "mel_heat_destroy"]
@@ -180,6 +181,8 @@ def load_library(path: str = LIB_PATH):
                                        C.POINTER(C.c_float), u64]),
         "mel_dataset_close": (None, [vp]),
         "mel_params_copy": (C.c_int, [vp, vp]),
+        "mel_create_virtual": (C.c_int, [C.POINTER(_Config), C.c_int, C.c_int, vp, C.POINTER(vp)]),
+        "surrogate_step_virtual": (C.c_int, [C.POINTER(vp), C.c_int, C.POINTER(C.c_double)]),
         "reservoir_put_generated": (C.c_int, [vp, vp, C.POINTER(u32), C.POINTER(C.c_float), C.POINTER(u32), u32,
                                               C.POINTER(u32)]),
         "mel_heat_create": (C.c_int, [u32, u32, C.c_double, C.c_double, C.c_double, C.POINTER(vp)]),
@@ -266,6 +269,18 @@ class Context:
         self.lib.mel_param_layout(self.h, C.byref(n), shapes, C.byref(tot))
         self.shapes = [(shapes[2 * i], shapes[2 * i + 1]) for i in range(n.value)]
         self.n_params = tot.value
+
+    @classmethod
+    def _from_handle(cls, cfg: Config, h, lib):
+        self = cls.__new__(cls)
+        self.lib, self.cfg, self._c, self.h = lib, cfg, cfg.to_c(), h
+        n = C.c_uint32()
+        shapes = (C.c_uint32 * 12)()
+        tot = C.c_uint64()
+        lib.mel_param_layout(h, C.byref(n), shapes, C.byref(tot))
+        self.shapes = [(shapes[2 * i], shapes[2 * i + 1]) for i in range(n.value)]
+        self.n_params = tot.value
+        return self
 
     # -- lifecycle -------------------------------------------------------------------
     def close_ctx(self):
@@ -455,6 +470,42 @@ class Context:
         n = C.c_uint64()
         self._check(self.lib.mel_launch_count(self.h, C.byref(n)))
         return n.value
+
+
+class VirtualGroup:
+    """`world` virtual ranks on one device (include/mel.h mel_create_virtual): .ctx[r] is
+    rank r's Context (puts, samples, state, stats as usual); step() is the collective
+    surrogate_step_virtual."""
+
+    def __init__(self, cfg: Config, world: int, device: int = 0, stream: int | None = None):
+        self.lib = load_library()
+        self.cfg, self.world = cfg, world
+        self._c = cfg.to_c()
+        hs = (C.c_void_p * world)()
+        r = self.lib.mel_create_virtual(C.byref(self._c), world, device, C.c_void_p(stream) if stream else None, hs)
+        if r != OK:
+            raise MelError(r, "mel_create_virtual failed (see stderr)")
+        self._hs = hs
+        self.ctx = [Context._from_handle(cfg, C.c_void_p(hs[q]), self.lib) for q in range(world)]
+        self.step_calls = 0
+
+    def step(self, want_loss: bool = True):
+        loss = C.c_double()
+        r = self.lib.surrogate_step_virtual(self._hs, self.world, C.byref(loss) if want_loss else None)
+        self.ctx[0]._check(r, (OK, EAGAIN, EOS))
+        self.step_calls += 1
+        return r, (loss.value if (want_loss and r == OK) else None)
+
+    def close(self):
+        for c in getattr(self, "ctx", []):
+            c.close_ctx()
+        self.ctx = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Ingest:

@@ -56,12 +56,24 @@ def rel_norm(a, b):
     return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))
 
 
+def tile_errors(a, b, rows_per_tile=128):
+    """W_L (rows = output neurons) compared per 128-row tile (one K1 tile / one exchange
+    unit): the worst tile's relative norm error and the element-wise max abs error."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    a2, b2 = a.reshape(a.shape[0], -1), b.reshape(b.shape[0], -1)
+    worst = 0.0
+    for r0 in range(0, a2.shape[0], rows_per_tile):
+        worst = max(worst, rel_norm(a2[r0:r0 + rows_per_tile], b2[r0:r0 + rows_per_tile]))
+    return worst, float(np.max(np.abs(a2 - b2))) if a2.size else 0.0
+
+
 def replay_parity(ctx, wl, table, ops, storage=0, seed=1, reanchor=True, max_train_steps=None,
                   on_step=None, check_every_sample=True, policy=0):
     """Drive ctx (world 1) and an oracle reservoir with the same op-log.  Returns a
     report dict; asserts bit-exact sampling on the way."""
     res = ores.Reservoir(wl.capacity, wl.threshold, wl.n_field, seed=seed, rank=0, storage=storage, policy=policy)
-    report = dict(loss_err=[], w_err=[], steps=0, samples=0, eagain=0)
+    report = dict(loss_err=[], w_err=[], tile_err=[], max_abs=[], steps=0, samples=0, eagain=0)
     last_slots = []
     S_host = 0
     k_host = 0
@@ -105,7 +117,11 @@ def replay_parity(ctx, wl, table, ops, storage=0, seed=1, reanchor=True, max_tra
                     tensors_f64(before["p"]), tensors_f64(before["m"]), tensors_f64(before["v"]),
                     before["k"], before["S"], [(xn, tn)], wl.n_field)
                 report["loss_err"].append(abs(loss_g - loss_o) / loss_o)
-                report["w_err"].append(max(rel_norm(a, b) for a, b in zip(tensors_f64(after["p"]), p_o)))
+                got = tensors_f64(after["p"])
+                report["w_err"].append(max(rel_norm(a, b) for a, b in zip(got, p_o)))
+                te, ma = tile_errors(got[-2], p_o[-2])          # W_L per 128-row tile
+                report["tile_err"].append(te)
+                report["max_abs"].append(ma)
             if on_step is not None:
                 on_step(ctx, res, loss_g, s)
             report["steps"] += 1

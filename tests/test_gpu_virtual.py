@@ -1,0 +1,130 @@
+"""Data-parallel parity on ONE GPU through virtual ranks (include/mel.h mel_create_virtual;
+SURVEY 4.2 T3').  R ranks live on one device: each has its own reservoir fed by its routed
+share of the clients ((sim + t) mod R), draws its own batch, and the collective step
+("the locally computed vector of weight updates is all-reduced") runs as ONE K1 launch
+over every rank's tiles -- in bf16 mode the in-kernel exchange itself: dW tiles TMA-stored /
+reduce-added into the owner rank's acc, the owner's counter bumped with red.release.sys and
+awaited with ld.acquire.sys, owner-side fused Adam, the new bf16 shadow rows pushed to every
+rank -- with the small region and [SSE, n] summed in rank order on the device.
+
+Checked against the oracle's R-rank step (oracle.trainer.one_step_from_state, re-anchored
+on the GPU state before each step): per-rank sampled slots bit-exact, global loss and every
+weight tensor within the north-star tolerance, W_L per 128-row tile (so a tile the exchange
+dropped cannot hide in a norm), replicas bitwise identical, reservoirs bit-exact."""
+import hashlib
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+from harness import FieldTable, compare_reservoir, make_config, rel_norm, tensors_f64, tile_errors
+from mel_inputs import design
+from oracle import mlp, reservoir as ores, trainer as otr
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu():
+    import torch
+    return torch.cuda.is_available()
+
+
+def run_virtual(world, mode, max_steps=5, wl=None, reanchor=True):
+    from paper_2309_16743_b200 import mel
+    flags = mel.FLAG_FP32_EXCHANGE if mode.endswith("-fp32x") else 0
+    if mode.startswith("fp32"):
+        wl = wl or replace(design.TINY_EVICT, world=world, puts_per_step=10)
+        prec = store = 0
+    else:
+        wl = wl or replace(design.MEDIUM, name="medium-bf16-vr", capacity=600, threshold=100, sims=30, world=world,
+                           batch=128, puts_per_step=60)
+        prec = store = 1
+    table = FieldTable(wl)
+    vg = mel.VirtualGroup(make_config(wl, precision=prec, storage=store, flags=flags), world, device=0)
+    res = [ores.Reservoir(wl.capacity, wl.threshold, wl.n_field, seed=1, rank=r, storage=store) for r in range(world)]
+    batches = [[] for _ in range(world)]
+    rep = dict(steps=0, loss_err=[], w_err=[], tile_err=[], max_abs=[], losses=[])
+    for op in design.build_oplog(wl):
+        kind = op[0]
+        if kind == "PUT":
+            _, r, s, t = op
+            res[r].put(s, t, table.Xs(s), table.field(s, t))
+            assert vg.ctx[r].put(s, t, table.Xs(s), table.field(s, t)) == 0
+        elif kind == "CLOSE":
+            res[op[1]].close()
+            vg.ctx[op[1]].close()
+        elif kind == "SAMPLE":
+            r = op[1]
+            st_o, sl_o = res[r].sample(wl.batch)
+            batches[r] = list(sl_o)
+            st_g, sl_g, n = vg.ctx[r].sample(want_slots=True)
+            assert st_g == st_o and list(sl_g) == list(sl_o), (r, st_g, st_o)
+        elif kind == "STEP":
+            n_tot = sum(len(b) for b in batches)
+            before = vg.ctx[0].get_state() if (n_tot and reanchor) else None
+            st_g, loss_g = vg.step(want_loss=True)
+            if n_tot == 0:
+                done = all(r_.over and r_.p == 0 for r_ in res)
+                assert st_g == (2 if done else 1), (st_g, done)
+                if done:
+                    break
+                continue
+            assert st_g == 0
+            rep["losses"].append(loss_g)
+            if reanchor:
+                rb = []
+                for r in range(world):
+                    if batches[r]:
+                        s = np.asarray(batches[r])
+                        rb.append((mlp.normalise_inputs(res[r].X[s], res[r].t[s], wl.tau),
+                                   ores.stored_to_f64(res[r].payload[s], store)))
+                    else:
+                        rb.append(None)
+                states = [vg.ctx[r].get_state() for r in range(world)]
+                hashes = {hashlib.sha256(b"".join(x.tobytes() for x in st["p"])).hexdigest() for st in states}
+                assert len(hashes) == 1, "replicas diverged"
+                after = states[0]
+                assert after["k"] == before["k"] + 1 and after["S"] == before["S"] + n_tot
+                loss_o, p_o, _, _, _ = otr.one_step_from_state(tensors_f64(before["p"]), tensors_f64(before["m"]),
+                                                                tensors_f64(before["v"]), before["k"], before["S"], rb,
+                                                                wl.n_field)
+                got = tensors_f64(after["p"])
+                rep["loss_err"].append(abs(loss_g - loss_o) / loss_o)
+                rep["w_err"].append(max(rel_norm(a, b) for a, b in zip(got, p_o)))
+                te, ma = tile_errors(got[-2], p_o[-2])
+                rep["tile_err"].append(te)
+                rep["max_abs"].append(ma)
+            batches = [[] for _ in range(world)]
+            rep["steps"] += 1
+            if max_steps and rep["steps"] >= max_steps:
+                break
+    for r in range(world):
+        compare_reservoir(vg.ctx[r], res[r], store)
+    vg.close()
+    return rep
+
+
+@pytest.mark.parametrize("world,mode", [(2, "fp32"), (4, "fp32"), (2, "bf16"), (4, "bf16"), (8, "bf16"),
+                                        (2, "bf16-fp32x"), (4, "bf16-fp32x"), (8, "bf16-fp32x")])
+def test_virtual_rank_parity(world, mode):
+    """fp32: the flat-gradient all-reduce, re-anchored at 1e-5 (north star).  bf16: the
+    in-kernel exchange (bf16 contributions by default, reading R22; -fp32x: fp32), loss within
+    2e-2, weights 1e-3 per tensor and 5e-3 per W_L tile."""
+    if not _gpu():
+        pytest.skip("needs a GPU")
+    rep = run_virtual(world, mode)
+    fp32 = mode.startswith("fp32")
+    tol_l, tol_w, tol_t = (1e-5, 1e-5, 1e-5) if fp32 else (2e-2, 1e-3, 5e-3)
+    print(world, mode, "steps", rep["steps"], "loss err %.2e" % max(rep["loss_err"]), "w err %.2e" % max(rep["w_err"]),
+          "tile err %.2e" % max(rep["tile_err"]), "max abs %.2e" % max(rep["max_abs"]))
+    assert rep["steps"] >= 4
+    assert max(rep["loss_err"]) <= tol_l and max(rep["w_err"]) <= tol_w and max(rep["tile_err"]) <= tol_t, rep
+
+
+def test_virtual_rank_to_eos_fp32():
+    """Two virtual ranks through reception, close and drain to the global EOS (reading R11:
+    unequal drains, a rank with nothing left contributes 0 samples), re-anchored every step."""
+    if not _gpu():
+        pytest.skip("needs a GPU")
+    rep = run_virtual(2, "fp32", max_steps=None)
+    assert rep["steps"] > 10 and max(rep["loss_err"]) <= 1e-5 and max(rep["w_err"]) <= 1e-5, rep
