@@ -59,7 +59,8 @@ enum mel_status {
   MEL_ECUDA = -4,     /* CUDA error (context poisoned)                                 */
   MEL_ENCCL = -5,     /* NCCL error (context poisoned)                                 */
   MEL_ENOMEM = -6,    /* device allocation failed                                      */
-  MEL_ENONFINITE = -7 /* loss not finite                                               */
+  MEL_ENONFINITE = -7 /* step skipped: a batch held non-finite inputs, or the loss is not
+                         finite (see surrogate_step)                                    */
 };
 
 enum mel_precision {
@@ -267,15 +268,23 @@ int reservoir_sample_batch(mel_ctx* ctx, int32_t* slots_host, uint32_t* n_host);
  * Returns MEL_OK, MEL_EAGAIN (no rank had samples: nothing done -- the parameters,
  * moments and step counters are unchanged; at world 1 the call launches no training
  * kernel at all, only the record of its status for surrogate_step_result, and
- * synchronises), MEL_EOS (every rank closed and drained), MEL_ENONFINITE (loss not
- * finite), errors. */
+ * synchronises), MEL_EOS (every rank closed and drained), MEL_ENONFINITE, errors.
+ * Non-finite values: a put whose X or field holds NaN / inf marks its slot at commit; a
+ * step whose batch (on any rank) contains such a slot updates nothing -- parameters,
+ * moments, step and sample counters unchanged -- and returns MEL_ENONFINITE (also reported
+ * as status 3 by surrogate_step_result; not a poisoning error, the next step trains).  A
+ * non-finite loss from finite inputs (arithmetic overflow) also returns MEL_ENONFINITE and
+ * skips the update of the head and biases, but the output layer's Adam runs inside K1
+ * before the global loss exists: there, elements whose gradient is not finite keep their
+ * value (every Adam kernel applies that rule) and the rest are updated. */
 int surrogate_step(mel_ctx* ctx, double* loss_host);
 
 /* Result of an earlier surrogate_step call without draining the stream: `call` is the
  * 0-based index of that call on this context, one of the last 16.  Waits only until that
  * step's kernels have finished (so a producer loop can read step i-1's loss while step i
  * runs), then returns its global mean loss (loss_host) and status (status_host: 0 trained,
- * 1 no rank had samples).  MEL_EINVAL for a call index out of range. */
+ * 1 no rank had samples, 3 skipped: non-finite inputs or loss, see surrogate_step).
+ * MEL_EINVAL for a call index out of range. */
 int surrogate_step_result(mel_ctx* ctx, uint64_t call, double* loss_host, int* status_host);
 
 /* Forward-only validation of n samples given on the host: X_host n x 5

@@ -20,6 +20,8 @@ struct ResDev {
   uint32_t n_last;     // size of the last batch (0 = EAGAIN / empty)
   uint32_t n_plan;     // entries committed by the last commit
   uint32_t head;       // FIFO: ring position of the oldest item
+  uint32_t bad_batch;  // the current batch holds an item with non-finite X or field values
+  uint32_t pad0;
   uint64_t hist[HIST_BINS];
 };
 
@@ -31,7 +33,7 @@ struct Mirror {
   uint64_t adam_k, samples;
   double loss;
   double n_total;
-  int32_t status;      // step: 0 ok, 1 skip (no samples)
+  int32_t status;      // step: 0 ok, 1 skip (no samples), 3 skipped: non-finite inputs or loss
   uint32_t pad;
   // per-call results of the last MEL_RESULT_RING surrogate_step calls (slot = call % ring),
   // read by surrogate_step_result without draining the stream
@@ -70,6 +72,7 @@ struct ResArgs {
   uint64_t* put_seq;         // [C]
   uint32_t* bitmap;          // [ceil(C/32)]
   uint32_t* pos;             // [C]
+  uint32_t* bad;             // [C] slot holds non-finite X or field values (set at commit)
   void* payload;             // [C][Npad] f32 or bf16
   uint32_t C, theta;
   uint64_t Npad;

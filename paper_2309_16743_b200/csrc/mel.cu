@@ -857,6 +857,8 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
   DALLOC(a.bitmap, (C + 31) / 32);
   CK(cudaMemset(a.bitmap, 0, sizeof(uint32_t) * ((C + 31) / 32)));
   DALLOC(a.pos, C);
+  DALLOC(a.bad, C);
+  CK(cudaMemset(a.bad, 0, sizeof(uint32_t) * C));
   const size_t esz = g->storage == MEL_STORE_F32 ? 4 : 2;
   {
     void* pl = nullptr;
@@ -1022,7 +1024,7 @@ void mel_destroy(mel_ctx* c) {
   drain_timers(c);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   void* ptrs[] = {c->d_st, (void*)c->ra.st_field, c->ra.meta, c->ra.seen, c->ra.put_seq,
-                  c->ra.bitmap, c->ra.pos, c->ra.payload, c->ra.plan, c->d_slots, c->d_p, c->d_m, c->d_v, c->d_g,
+                  c->ra.bitmap, c->ra.pos, c->ra.bad, c->ra.payload, c->ra.plan, c->d_slots, c->d_p, c->d_m, c->d_v, c->d_g,
                   c->d_shadow[0], c->d_shadow[1], c->d_xn, c->d_z[0], c->d_z[1], c->d_h[0], c->d_h[1], c->d_dz[0],
                   c->d_dz[1], c->d_dy, c->d_part, c->d_sse_part, c->d_sd, c->d_eval_x, c->d_eval_t, c->d_eval_y,
                   c->d_eval_f, c->d_eval_z[0], c->d_eval_z[1], c->d_eval_h[0], c->d_eval_h[1], c->d_eval_xn,
@@ -1561,6 +1563,8 @@ int surrogate_step(mel_ctx* c, double* loss_host) {
   if (!need_sync) return MEL_OK;
   if ((r = sync_stream(c))) return r;
   const Mirror& m = *c->h_mirror;
+  if (m.status == 3)
+    return fail(c, MEL_ENONFINITE, "step skipped: non-finite inputs in a batch or a non-finite loss (%g)", m.loss);
   if (m.status == 1) {
     bool eos = c->closed && m.over && m.p == 0;
     if (c->world > 1) {
@@ -1644,6 +1648,8 @@ int surrogate_step_virtual(mel_ctx* const* cs, int world, double* loss_host) {
   CK(cudaStreamSynchronize(s));
   for (int q = 0; q < world; ++q) cs[q]->known_consumed = cs[q]->h_mirror->consumed;
   const Mirror& m = *c->h_mirror;
+  if (m.status == 3)
+    return fail(c, MEL_ENONFINITE, "step skipped: non-finite inputs in a batch or a non-finite loss (%g)", m.loss);
   if (m.status == 1) {
     bool eos = true;
     for (int q = 0; q < world; ++q) {

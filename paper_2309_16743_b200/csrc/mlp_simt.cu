@@ -230,7 +230,8 @@ __global__ void reduce_local_kernel(StepDev* sd, const double* parts, int n_part
     if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) { sd->red[0] = s[0]; sd->red[1] = (double)st->n_last; }
+  // a batch with non-finite inputs contributes NaN to the global count: every rank skips
+  if (threadIdx.x == 0) { sd->red[0] = s[0]; sd->red[1] = st->bad_batch ? nan("") : (double)st->n_last; }
 }
 
 __global__ void step_finalize_kernel(StepDev* sd, double n_field, double lr0, double lr_min, uint64_t halving,
@@ -238,7 +239,16 @@ __global__ void step_finalize_kernel(StepDev* sd, double n_field, double lr0, do
   pdl_enter();
   const double sse = sd->red[0], n = sd->red[1];
   st->n_last = 0;                       // a batch is consumed by exactly one step
+  st->bad_batch = 0;
   mirror->n_last = 0;
+  if (isnan(n) || (n > 0.0 && !isfinite(sse))) {
+    // some rank's batch held non-finite inputs (n = NaN: nothing was updated, reading of
+    // the ABI's "state unchanged"), or the loss itself is not finite: skip the update
+    sd->skip = 1; sd->nonfinite = 1;
+    mirror->status = 3; mirror->n_total = n; mirror->loss = sse;
+    mirror->ring_status[slot] = 3; mirror->ring_loss[slot] = nan("");
+    return;
+  }
   if (n <= 0.0) {
     sd->skip = 1;
     mirror->status = 1; mirror->n_total = 0.0;
@@ -269,8 +279,8 @@ __global__ void step_finalize_kernel(StepDev* sd, double n_field, double lr0, do
 __global__ void step_prepare_kernel(StepDev* sd, const ResDev* st, double n_field, double lr0, double lr_min,
                                     uint64_t halving, double b1, double b2, int global_n) {
   pdl_enter();
-  const double n = global_n ? sd->n_glob : (double)st->n_last;
-  if (n <= 0.0) { sd->skip = 1; return; }
+  const double n = global_n ? sd->n_glob : (st->bad_batch ? nan("") : (double)st->n_last);
+  if (!(n > 0.0)) { sd->skip = 1; return; }            // no samples, or non-finite inputs (NaN)
   sd->skip = 0;
   sd->scale = (float)(1.0 / (n_field * n));
   sd->lr = (float)fmax(lr_min, lr0 * exp2(-(double)(sd->S / halving)));
@@ -288,6 +298,7 @@ __device__ __forceinline__ void adam4(float4& pp, float4& mm, float4& vv, const 
   float* P = &pp.x; float* Mv = &mm.x; float* V = &vv.x; const float* G = &gg.x;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
+    if (!isfinite(G[c])) continue;      // a non-finite gradient element leaves p, m, v as they are
     const float gr = G[c] * scale;
     Mv[c] = fmaf(b1, Mv[c], (1.f - b1) * gr);
     V[c] = fmaf(b2, V[c], (1.f - b2) * gr * gr);
@@ -471,7 +482,7 @@ void step_prepare(StepDev* sd, const ResDev* st, double n_field, double lr0, dou
 }
 
 __global__ void stage_count_kernel(StepDev* sd, const ResDev* st) {
-  pdl_enter(); sd->n_glob = (double)st->n_last; }
+  pdl_enter(); sd->n_glob = st->bad_batch ? nan("") : (double)st->n_last; }
 
 void stage_count(StepDev* sd, const ResDev* st, cudaStream_t s) { launch_pdl(stage_count_kernel, dim3(1), dim3(1), 0, s, sd, st); }
 

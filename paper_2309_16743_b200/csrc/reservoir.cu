@@ -164,6 +164,10 @@ commit_ctrl(ResArgs a, uint64_t tail, uint32_t closed) {
       atomicAdd(reinterpret_cast<unsigned long long*>(&st->hist[sc < HIST_BINS ? sc : HIST_BINS - 1]), 1ull);
     }
     a.meta[j] = a.st_meta[ej.x];
+    {
+      const float* X = a.st_meta[ej.x].X;
+      a.bad[j] = (isfinite(X[0]) && isfinite(X[1]) && isfinite(X[2]) && isfinite(X[3]) && isfinite(X[4])) ? 0u : 1u;
+    }
     a.seen[j] = 0;
     a.put_seq[j] = q0 + i;
     a.plan[i] = make_uint2(ej.x, j);
@@ -198,6 +202,11 @@ commit_copy(ResArgs a) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
       float4 v = __ldg(src + i);
       float o[4] = {v.x, v.y, v.z, v.w};
+      // a non-finite value marks the slot (its batches are skipped, surrogate_step ->
+      // MEL_ENONFINITE); the padding lanes past N never count
+      if (!(isfinite(v.x) || 4 * i >= a.N) || !(isfinite(v.y) || 4 * i + 1 >= a.N) ||
+          !(isfinite(v.z) || 4 * i + 2 >= a.N) || !(isfinite(v.w) || 4 * i + 3 >= a.N))
+        atomicOr(&a.bad[ej.y], 1u);
 #pragma unroll
       for (int c = 0; c < 4; ++c) o[c] = (4 * i + c < a.N) ? normalise_rn(o[c], a.lo, a.span) : 0.f;
       if (STORAGE == 0) {
@@ -345,6 +354,7 @@ __global__ void gather_inputs(ResArgs a, const int32_t* slots, uint32_t B, uint3
   const uint32_t n = a.st->n_last;
   float out[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (b < n) {
+    if (a.bad[slots[b]]) atomicOr(&a.st->bad_batch, 1u);     // reset by step_finalize
     const SlotMeta m = a.meta[slots[b]];
 #pragma unroll
     for (int c = 0; c < 5; ++c) out[c] = normalise_rn(m.X[c], a.lo, a.span);

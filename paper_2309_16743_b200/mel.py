@@ -111,6 +111,8 @@ def _ingest_sigs():
 
 def _bind(lib, sig):
     for name, (res, args) in sig.items():
+        if os.environ.get("MEL_LIB") and not hasattr(lib, name):
+            continue                     # an older A/B build without this entry point
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
@@ -363,8 +365,8 @@ class Context:
     def step(self, want_loss: bool = True):
         loss = C.c_double()
         r = self.lib.surrogate_step(self.h, C.byref(loss) if want_loss else None)
-        self._check(r, (OK, EAGAIN, EOS))
         self.step_calls = getattr(self, "step_calls", 0) + 1
+        self._check(r, (OK, EAGAIN, EOS))
         return r, (loss.value if (want_loss and r == OK) else None)
 
     def step_result(self, call: int):
@@ -492,8 +494,8 @@ class VirtualGroup:
     def step(self, want_loss: bool = True):
         loss = C.c_double()
         r = self.lib.surrogate_step_virtual(self._hs, self.world, C.byref(loss) if want_loss else None)
-        self.ctx[0]._check(r, (OK, EAGAIN, EOS))
         self.step_calls += 1
+        self.ctx[0]._check(r, (OK, EAGAIN, EOS))
         return r, (loss.value if (want_loss and r == OK) else None)
 
     def close(self):

@@ -57,6 +57,23 @@ def test_medium_geometry_with_evictions_reanchored(mel):
     compare_reservoir(ctx, rep["oracle_res"])
     assert rep["oracle_res"].evictions > 0
     assert max(rep["loss_err"]) <= 1e-5 and max(rep["w_err"]) <= 1e-5, (max(rep["loss_err"]), max(rep["w_err"]))
+    assert max(rep["tile_err"]) <= 1e-5, max(rep["tile_err"])
+
+
+@pytest.mark.slow
+def test_medium_config_fp32_1000_steps_reanchored(mel):
+    """SURVEY 8(c) O7 at BASELINE configs[1] as stated: medium (100x100 grid, tau 100, 1000
+    sims, 6-256-256-10^4, C = 50,000, theta = 8,333, B = 256), fp32 mode, every one of 1000
+    training steps re-anchored to the fp64 oracle step (loss and every tensor <= 1e-5, W_L per
+    128-row tile <= 1e-5, north star); sampled slots bit-exact on every SAMPLE."""
+    wl = design.MEDIUM
+    table = FieldTable(wl)
+    ctx = mel.Context(make_config(wl))
+    rep = replay_parity(ctx, wl, table, design.build_oplog(wl), max_train_steps=1000)
+    print("medium fp32: %d steps, loss err %.2e, w err %.2e, W_L tile err %.2e, max abs %.2e" %
+          (rep["steps"], max(rep["loss_err"]), max(rep["w_err"]), max(rep["tile_err"]), max(rep["max_abs"])))
+    assert rep["steps"] == 1000
+    assert max(rep["loss_err"]) <= 1e-5 and max(rep["w_err"]) <= 1e-5 and max(rep["tile_err"]) <= 1e-5
 
 
 @pytest.mark.parametrize("seed", [3, 4])
