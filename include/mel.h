@@ -91,7 +91,9 @@ typedef struct {
   uint32_t hidden[2];          /* hidden widths; {256,256}; tiny {32,0}          */
   uint32_t capacity;           /* C, reservoir slots per rank (6000)              */
   uint32_t threshold;          /* theta, watermark (1000); require theta < C      */
-  uint32_t batch;              /* B per rank (10; bench: 1024)                    */
+  uint32_t batch;              /* B per rank (10; bench: 1024); any B >= 1 -- the
+                                  bf16 kernels run it padded to whole 64-row chunks,
+                                  the padding rows masked out of loss and gradients   */
   uint32_t steps_per_sim;      /* tau, used for the input t/tau (100)             */
   float temp_lo, temp_hi;      /* normalisation range, 100 / 500 K               */
   uint32_t precision;          /* enum mel_precision                                     */
@@ -189,11 +191,16 @@ int mel_set_state(mel_ctx* ctx, const mel_state_view* in);
  * is committed to a slot at the next commit point (start of
  * reservoir_sample_batch, or reservoir_close).  field_on_device = 0: field is
  * host memory, copied before return (pinned memory makes the copy asynchronous);
- * 1: device pointer, read in stream order by the commit that consumes the item -- zero
- * copy when it is 16-byte aligned and n_field % 4 == 0, else copied on the stream at the
- * call; either way it must stay valid and unchanged until the next mel_sync().  Errors: MEL_ECLOSED after close,
- * MEL_EAGAIN when the staging ring is full (the caller retries after sampling),
- * MEL_EINVAL. */
+ * 1: device pointer on this context's GPU, copied into the staging ring on the context's
+ * stream at the call (the buffer is free once the stream has passed that point: at once
+ * for a caller on the same stream; a producer on another stream orders its writes first,
+ * e.g. with mel_stream_wait_event); 2: device pointer, ZERO COPY -- the commit that
+ * consumes the item reads the caller's field in stream order, which under back-pressure
+ * (u == C) may be several sample calls later, so the buffer must stay valid and
+ * unchanged until the item is committed AND that commit has run: until reservoir_stats
+ * (which synchronises) reports pending == 0 (needs 16-byte alignment and n_field % 4 == 0,
+ * else it is copied as with 1).  Errors: MEL_ECLOSED after close, MEL_EAGAIN when the
+ * staging ring is full (the caller retries after sampling), MEL_EINVAL. */
 int reservoir_put(mel_ctx* ctx, uint32_t sim_id, uint32_t t, const float X_host[5],
                   const float* field, int field_on_device);
 
@@ -317,6 +324,10 @@ int mel_params_copy(mel_ctx* dst, mel_ctx* src);
 
 /* Waits for all work queued on the context's stream. */
 int mel_sync(mel_ctx* ctx);
+
+/* Orders the context's stream after a CUDA event (cudaEvent_t) recorded by the caller, e.g.
+ * on the stream that produced a device field before reservoir_put(..., 1 or 2). */
+int mel_stream_wait_event(mel_ctx* ctx, void* cuda_event);
 
 /* Virtual ranks (test mode; "the locally computed vector of weight updates is
  * all-reduced", SURVEY 4.2 T3'): `world` (2..8) ranks on ONE device, so that the

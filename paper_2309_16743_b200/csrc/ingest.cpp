@@ -117,6 +117,7 @@ struct mel_client {
   uint32_t id = 0, world = 0, n_field = 0;
   bool finalized = false;
   bool die_after_claim = false;   // fault injection for tests: MEL_INGEST_FAULT=die_after_claim
+  bool die_after_pid = false;     //   ... MEL_INGEST_FAULT=die_after_pid (slot reserved, ticket not taken)
 };
 
 namespace {
@@ -297,6 +298,7 @@ int mel_client_open(const char* name, uint32_t world, uint32_t client_id, mel_cl
   c->world = world;
   const char* fault = getenv("MEL_INGEST_FAULT");
   c->die_after_claim = fault && strcmp(fault, "die_after_claim") == 0;
+  c->die_after_pid = fault && strcmp(fault, "die_after_pid") == 0;
   for (uint32_t r = 0; r < world; ++r) {
     Mapping m;
     int st = map_file(seg_path(name, r), false, 0, &m);
@@ -335,13 +337,33 @@ int client_push(mel_client* c, uint32_t r, uint32_t timeout_us, F&& fill) {
     const uint64_t seq = s->seq.load(std::memory_order_acquire);
     const int64_t dif = (int64_t)(seq - pos);
     if (dif == 0) {
-      if (h->enq.compare_exchange_weak(pos, pos + 1, std::memory_order_acq_rel, std::memory_order_relaxed)) {
-        s->pid.store((int32_t)getpid(), std::memory_order_relaxed);
+      // reserve the slot with our pid first (a free slot has pid 0; a reservation left by a
+      // process that died before taking the ticket is taken over), then take the ticket:
+      // a claimed ticket therefore always names its claimant, so the server can tell a
+      // claimant that died before publishing (mel_ingest_next skips its ticket)
+      const int32_t me = (int32_t)getpid();
+      int32_t cur = s->pid.load(std::memory_order_relaxed);
+      if (cur != 0 && cur != me &&
+          (!process_gone(cur) || h->enq.load(std::memory_order_acquire) != pos)) {
+        // a live client's reservation, or a ticket a dead client took (the server skips it)
+        pos = h->enq.load(std::memory_order_relaxed);
+        continue;
+      }
+      if (!s->pid.compare_exchange_strong(cur, me, std::memory_order_acq_rel, std::memory_order_relaxed)) {
+        pos = h->enq.load(std::memory_order_relaxed);
+        continue;
+      }
+      if (c->die_after_pid) _exit(4);                     // a crash between reservation and ticket
+      uint64_t expect = pos;
+      if (h->enq.compare_exchange_strong(expect, pos + 1, std::memory_order_acq_rel, std::memory_order_relaxed)) {
         if (c->die_after_claim) _exit(3);                 // a client crash between claim and publish
         fill(s, m.field(s));
         s->seq.store(pos + 1, std::memory_order_release);
         return ST_OK;
       }
+      int32_t mine = me;                                  // lost the ticket: drop the reservation
+      s->pid.compare_exchange_strong(mine, 0, std::memory_order_acq_rel, std::memory_order_relaxed);
+      pos = expect;
     } else if (dif < 0) {                                 // ring full: the slot is a lap behind
       if (!w.again()) return ST_EAGAIN;
       pos = h->enq.load(std::memory_order_relaxed);

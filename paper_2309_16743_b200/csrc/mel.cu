@@ -60,6 +60,8 @@ struct mel_ctx {
   int L = 0;                       // number of weight layers
   uint32_t dims[4] = {0, 0, 0, 0}; // [6, hidden..., N]
   uint32_t N = 0, B = 0, C = 0, Klast = 0, hmax = 0;
+  uint32_t Bs = 0;                 // batch the sampler draws (cfg.batch); B = rows the kernels run
+                                   // (bf16: Bs padded to the 64-row K1 chunk, rows >= n masked)
   uint64_t Npad = 0;
   uint64_t off[2 * 3] = {};        // tensor offsets in the flat buffers
   uint64_t cnt[2 * 3] = {};
@@ -285,7 +287,6 @@ int validate(const mel_config* g, int world, mel_ctx* c) {
   const uint32_t klast = g->hidden[1] ? g->hidden[1] : g->hidden[0];
   if (g->precision == MEL_BF16) {
     if (klast % 64 != 0 || klast > 256) return fail(c, MEL_EINVAL, "bf16 mode needs the last hidden width in {64,128,192,256}");
-    if (g->batch % 64 != 0) return fail(c, MEL_EINVAL, "bf16 mode needs batch %% 64 == 0");
     if (g->storage != MEL_STORE_BF16) return fail(c, MEL_EINVAL, "bf16 mode stores targets as bf16 (MEL_STORE_BF16)");
   }
   if (world < 1) return fail(c, MEL_EINVAL, "world must be >= 1");
@@ -812,7 +813,8 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
   if (g->hidden[1]) c->dims[nd++] = g->hidden[1];
   c->dims[nd++] = g->n_field;
   c->L = nd - 1;
-  c->N = g->n_field; c->B = g->batch; c->C = g->capacity;
+  c->N = g->n_field; c->Bs = g->batch; c->C = g->capacity;
+  c->B = g->precision == MEL_BF16 ? (g->batch + 63) / 64 * 64 : g->batch;
   // rows of W_L padded to 128 (UMMA M) x world (equal row shards under ZeRO)
   const uint64_t row_quant = 128ull * (uint64_t)c->world;
   c->Npad = ((uint64_t)c->N + row_quant - 1) / row_quant * row_quant;
@@ -1246,6 +1248,7 @@ static int put_impl(mel_ctx* c, uint32_t sim, uint32_t t, const float X[5], cons
                     bool zero_copy);
 
 int reservoir_put(mel_ctx* c, uint32_t sim, uint32_t t, const float X[5], const float* field, int on_device) {
+  if (on_device < 0 || on_device > 2) return fail(c, MEL_EINVAL, "field_on_device must be 0, 1 or 2");
   return put_impl(c, sim, t, X, field, on_device, true);
 }
 
@@ -1266,9 +1269,9 @@ static int put_impl(mel_ctx* c, uint32_t sim, uint32_t t, const float X[5], cons
   c->h_stmeta[e] = m;
   float* dst = const_cast<float*>(c->ra.st_field) + (uint64_t)e * c->Npad;
   c->h_stsrc[e] = nullptr;
-  if (on_device && zero_copy && c->N % 4 == 0 && ((uintptr_t)field & 15) == 0) {
-    // zero copy: the commit that consumes this entry reads the caller's field in stream
-    // order (the mel.h contract keeps it valid until the next mel_sync)
+  if (on_device == 2 && zero_copy && c->N % 4 == 0 && ((uintptr_t)field & 15) == 0) {
+    // zero copy (opt-in): the commit that consumes this entry reads the caller's field in
+    // stream order; the mel.h contract keeps it valid until that commit has run
     c->h_stsrc[e] = field;
   } else if (on_device) {
     CK(cudaMemcpyAsync(dst, field, 4ull * c->N, cudaMemcpyDeviceToDevice, c->stream));
@@ -1373,21 +1376,21 @@ int surrogate_train_offline(mel_ctx* c, mel_dataset* d, uint64_t seed, uint32_t 
   if (steps_host) *steps_host = 0;
   if (!d) return fail(c, MEL_EINVAL, "null dataset");
   if (c->cfg.policy != MEL_FIFO) return fail(c, MEL_EINVAL, "offline training needs mel_config.policy = MEL_FIFO");
-  if (c->cfg.staging_entries < c->B) return fail(c, MEL_EINVAL, "offline training needs staging_entries >= batch");
+  if (c->cfg.staging_entries < c->Bs) return fail(c, MEL_EINVAL, "offline training needs staging_entries >= batch");
   if (mel_dataset_n_field(d) != c->N) return fail(c, MEL_EINVAL, "dataset n_field %u != %u", mel_dataset_n_field(d), c->N);
   if (c->closed) return fail(c, MEL_ECLOSED, "offline training after reservoir_close");
   const uint64_t count = mel_dataset_count(d);
-  const uint64_t nb_epoch = count / c->B;                    // the last partial batch is dropped (R24)
+  const uint64_t nb_epoch = count / c->Bs;                   // the last partial batch is dropped (R24)
   if (first_batch >= nb_epoch) return MEL_OK;
   if (n_batches > nb_epoch - first_batch) n_batches = (uint32_t)(nb_epoch - first_batch);
   std::vector<uint32_t> perm(count);
   mel_dataset_epoch_order(count, seed, epoch, perm.data());
-  const uint32_t* order = perm.data() + (uint64_t)first_batch * c->B;
-  const uint64_t total = (uint64_t)n_batches * c->B;
+  const uint32_t* order = perm.data() + (uint64_t)first_batch * c->Bs;
+  const uint64_t total = (uint64_t)n_batches * c->Bs;
   // records move in chunks through two pinned buffers: the loader threads read chunk q+1
   // while chunk q's fields are DMA-copied into the staging ring and the GPU trains
   if (!c->off_buf[0]) {
-    c->off_chunk = c->B < 64 ? c->B : 64;
+    c->off_chunk = c->Bs < 64 ? c->Bs : 64;
     for (int i = 0; i < 2; ++i) {
       CK(cudaHostAlloc((void**)&c->off_buf[i], (size_t)c->off_chunk * c->N * 4, cudaHostAllocDefault));
       CK(cudaEventCreateWithFlags(&c->off_ev[i], cudaEventDisableTiming));
@@ -1420,7 +1423,7 @@ int surrogate_train_offline(mel_ctx* c, mel_dataset* d, uint64_t seed, uint32_t 
       int r = reservoir_put(c, sim[b * chunk + k], tt[b * chunk + k], &X[5 * (b * chunk + k)],
                             c->off_buf[b] + (uint64_t)k * c->N, 0);
       if (r) return r;
-      if (++put % c->B == 0) {
+      if (++put % c->Bs == 0) {
         // the FIFO hands out exactly the B records just put, in epoch order
         if ((r = reservoir_sample_batch(c, nullptr, nullptr))) return r;
         if ((r = surrogate_step(c, nullptr))) return r;
@@ -1492,14 +1495,14 @@ int reservoir_sample_batch(mel_ctx* c, int32_t* slots_host, uint32_t* n_host) {
   if (r) return r;
   {
     Timer t(c, MEL_K_SAMPLE, 1);
-    launch_sample(c->ra, c->d_slots, c->B, c->stream);
+    launch_sample(c->ra, c->d_slots, c->Bs, c->stream);
   }
   r = check_launch(c, "sample");
   if (r) return r;
   // During reception the fill phase never blocks (u <= p < C), so p = min(C, puts)
   // at every commit point and the watermark gate is host-decidable.
   bool need_sync = slots_host || n_host || c->closed;
-  uint32_t n = c->B;
+  uint32_t n = c->Bs;
   if (!c->closed) {
     if (c->cfg.policy == MEL_RESERVOIR) {
       const uint64_t p = c->tail < c->C ? c->tail : c->C;
@@ -1509,7 +1512,7 @@ int reservoir_sample_batch(mel_ctx* c, int32_t* slots_host, uint32_t* n_host) {
       // buffer, or pending, and a commit fills the buffer up to C
       const uint64_t left = c->tail - c->drawn;
       const uint64_t p = left < c->C ? left : c->C;
-      const uint64_t need = c->cfg.policy == MEL_FIFO ? c->B : (uint64_t)c->cfg.threshold + c->B;
+      const uint64_t need = c->cfg.policy == MEL_FIFO ? c->Bs : (uint64_t)c->cfg.threshold + c->Bs;
       if (p < need) n = 0;
     }
   }
@@ -1823,6 +1826,13 @@ int mel_params_copy(mel_ctx* dst, mel_ctx* src) {
   CK(cudaStreamWaitEvent(src->stream, copied, 0));
   cudaEventDestroy(ready);
   cudaEventDestroy(copied);
+  return MEL_OK;
+}
+
+int mel_stream_wait_event(mel_ctx* c, void* cuda_event) {
+  GUARD(c);
+  if (!cuda_event) return fail(c, MEL_EINVAL, "null event");
+  CK(cudaStreamWaitEvent(c->stream, (cudaEvent_t)cuda_event, 0));
   return MEL_OK;
 }
 

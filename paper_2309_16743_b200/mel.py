@@ -38,7 +38,7 @@ EXPORTS = ["mel_config_default", "mel_nccl_unique_id", "mel_create", "mel_destro
            "reservoir_stats", "reservoir_dump", "mel_sync", "mel_kernel_time", "mel_kernel_time_reset",
            "mel_launch_count", "mel_set_flags", "mel_debug_counters", "reservoir_ingest",
            "surrogate_train_offline", "reservoir_put_generated", "mel_params_copy", "mel_create_virtual",
-           "surrogate_step_virtual"]
+           "surrogate_step_virtual", "mel_stream_wait_event"]
 # include/mel_heat.h (on-device heat-equation client)
 HEAT_EXPORTS = ["mel_heat_create", "mel_heat_basis_bytes", "mel_heat_grid", "mel_heat_tau", "mel_heat_fields",
                 "mel_heat_destroy"]
@@ -183,6 +183,7 @@ def load_library(path: str = LIB_PATH):
                                        C.POINTER(C.c_float), u64]),
         "mel_dataset_close": (None, [vp]),
         "mel_params_copy": (C.c_int, [vp, vp]),
+        "mel_stream_wait_event": (C.c_int, [vp, vp]),
         "mel_create_virtual": (C.c_int, [C.POINTER(_Config), C.c_int, C.c_int, vp, C.POINTER(vp)]),
         "surrogate_step_virtual": (C.c_int, [C.POINTER(vp), C.c_int, C.POINTER(C.c_double)]),
         "reservoir_put_generated": (C.c_int, [vp, vp, C.POINTER(u32), C.POINTER(C.c_float), C.POINTER(u32), u32,
@@ -258,6 +259,7 @@ class Context:
         self.lib = load_library()
         self.cfg = cfg
         self._c = cfg.to_c()
+        self._stream = stream
         h = C.c_void_p()
         idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         r = self.lib.mel_create(C.byref(self._c), rank, world, idbuf, device, C.c_void_p(stream) if stream else None,
@@ -276,6 +278,7 @@ class Context:
     def _from_handle(cls, cfg: Config, h, lib):
         self = cls.__new__(cls)
         self.lib, self.cfg, self._c, self.h = lib, cfg, cfg.to_c(), h
+        self._stream = None
         n = C.c_uint32()
         shapes = (C.c_uint32 * 12)()
         tot = C.c_uint64()
@@ -303,11 +306,26 @@ class Context:
         raise MelError(r, msg)
 
     # -- reservoir ---------------------------------------------------------------------
-    def put(self, sim: int, t: int, X, field) -> int:
+    def put(self, sim: int, t: int, X, field, zero_copy: bool = False) -> int:
+        """A torch CUDA tensor is copied on the context's stream at the call (after the
+        work torch's current stream has queued so far), or with zero_copy=True read in place
+        by the commit that consumes it: the tensor is then kept referenced here until
+        stats() shows no pending put (include/mel.h reservoir_put, field_on_device 2)."""
         Xa = np.ascontiguousarray(X, dtype=np.float32)
         if hasattr(field, "data_ptr"):                       # torch tensor
-            on_dev = 1 if field.is_cuda else 0
+            on_dev = (2 if zero_copy else 1) if field.is_cuda else 0
             ptr = C.c_void_p(field.data_ptr())
+            if field.is_cuda:
+                import torch
+                cur = torch.cuda.current_stream(field.device)
+                if cur.cuda_stream != getattr(self, "_stream", None):
+                    ev = torch.cuda.Event()
+                    ev.record(cur)
+                    self._check(self.lib.mel_stream_wait_event(self.h, C.c_void_p(ev.cuda_event)))
+                if zero_copy:
+                    if not hasattr(self, "_zc_refs"):
+                        self._zc_refs = []
+                    self._zc_refs.append(field)
         else:
             field = np.ascontiguousarray(field, dtype=np.float32)
             on_dev, ptr = 0, field.ctypes.data_as(C.c_void_p)
@@ -399,6 +417,8 @@ class Context:
         self._check(self.lib.reservoir_stats(self.h, C.byref(s)))
         d = {k: getattr(s, k) for k, _ in _Stats._fields_ if k != "hist"}
         d["hist"] = np.array(list(s.hist), dtype=np.int64)
+        if d.get("pending", 1) == 0:
+            self._zc_refs = []                    # every zero-copy put has been committed
         return d
 
     def dump(self, payload: bool = True) -> dict:

@@ -122,11 +122,12 @@ def test_random_schedules_with_backpressure_and_ring_wrap(mel, seed):
     assert e.value.code == mel.EPROTO
 
 
-@pytest.mark.parametrize("offset", [0, 1], ids=["zero-copy", "unaligned-copied"])
-def test_device_resident_puts_match_host_puts(mel, offset):
-    """Device puts: an aligned field is read by the commit straight from the caller's
-    buffer (zero copy); a 4-byte-offset one is copied at the call.  Both must equal the
-    host puts bit for bit."""
+@pytest.mark.parametrize("offset,zc", [(0, True), (1, True), (0, False)],
+                         ids=["zero-copy", "unaligned-copied", "copied"])
+def test_device_resident_puts_match_host_puts(mel, offset, zc):
+    """Device puts: with zero_copy an aligned field is read by the commit straight from the
+    caller's buffer (field_on_device 2); a 4-byte-offset one, or any without zero_copy, is
+    copied at the call.  All must equal the host puts bit for bit."""
     import torch
     wl = design.TINY_EVICT
     table = FieldTable(wl)
@@ -140,9 +141,33 @@ def test_device_resident_puts_match_host_puts(mel, offset):
         buf[offset:] = torch.from_numpy(f).cuda()
         keep.append(buf)
         torch.cuda.synchronize()
-        b.put(s, t, table.Xs(s), buf[offset:])
+        b.put(s, t, table.Xs(s), buf[offset:], zero_copy=zc)
         if t % 5 == 4:
             assert list(a.sample(True)[1]) == list(b.sample(True)[1])
+    da, db = a.dump(), b.dump()
+    for k in da:
+        assert np.array_equal(da[k], db[k]), k
+
+
+def test_copied_device_put_buffer_reusable_after_the_call(mel):
+    """field_on_device 1 (the default for torch tensors): the field is copied on the
+    context's stream at the call, so the caller may overwrite its buffer right after
+    (same stream order) -- the reservoir still holds the values put."""
+    import torch
+    wl = replace(design.TINY, capacity=16, threshold=2, batch=4)
+    table = FieldTable(wl)
+    stream = torch.cuda.Stream()
+    a = mel.Context(make_config(wl))
+    b = mel.Context(make_config(wl), stream=stream.cuda_stream)   # the producer's stream
+    with torch.cuda.stream(stream):
+        buf = torch.zeros(wl.n_field, dtype=torch.float32, device="cuda")
+        for (s, t) in design.stream_order(wl.sims, wl.tau)[:12]:
+            f = table.field(s, t)
+            a.put(s, t, table.Xs(s), f)
+            buf.copy_(torch.from_numpy(f).cuda())
+            b.put(s, t, table.Xs(s), buf)
+            buf.fill_(float("nan"))             # reused before any commit has run
+    a.sample(); b.sample()
     da, db = a.dump(), b.dump()
     for k in da:
         assert np.array_equal(da[k], db[k]), k

@@ -130,6 +130,19 @@ def test_client_dying_between_claim_and_publish_is_skipped(lib):
     ing.destroy()
 
 
+def test_client_dying_between_reservation_and_ticket_does_not_wedge(lib):
+    """A client killed after reserving a slot (pid written) but before taking the ticket:
+    the next client takes the reservation over and the ring keeps flowing."""
+    n, name = 32, _name()
+    ing = mel.Ingest(name, 0, n, slots=8, expected_clients=1)
+    assert _spawn(name, 1, 1, 0, 3, n, env={"MEL_INGEST_FAULT": "die_after_pid"}).wait(60) == 4
+    assert _spawn(name, 1, 2, 0, 3, n, finalize=True).wait(60) == 0
+    got = _drain(ing)
+    assert [(m["sim_id"], m["t"]) for m in got] == [(2, t) for t in range(3)]
+    assert ing.stats()["abandoned"] == 0
+    ing.destroy()
+
+
 def test_full_ring_and_protocol_errors(lib):
     n, name = 16, _name()
     ing = mel.Ingest(name, 0, n, slots=2)
