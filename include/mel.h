@@ -111,8 +111,9 @@ typedef struct {
 #define MEL_FLAG_TIMING 1u     /* record CUDA events around every kernel (bench roofline) */
 #define MEL_FLAG_UNFUSED_ADAM 8u /* world == 1, bf16: run Adam of W_L as its own kernel over a
                                     stored gradient instead of inside the output-layer kernel's
-                                    dW epilogue (the default there).  Read at
-                                    mel_create only.                                        */
+                                    dW epilogue (the default there from batch 256 on; below
+                                    it the separate kernel is already the default, DESIGN
+                                    §7).  Read at mel_create only.                          */
 #define MEL_FLAG_NCCL_EXCHANGE 16u /* world > 1, bf16: NCCL reduce-scatter of dW_L + sharded Adam
                                       kernel + shadow all-gather instead of the in-kernel NVLink
                                       exchange (the default when every GPU pair has peer access;
@@ -282,8 +283,9 @@ int reservoir_sample_batch(mel_ctx* ctx, int32_t* slots_host, uint32_t* n_host);
  * as status 3 by surrogate_step_result; not a poisoning error, the next step trains).  A
  * non-finite loss from finite inputs (arithmetic overflow) also returns MEL_ENONFINITE and
  * skips the update of the head and biases, but the output layer's Adam runs inside K1
- * before the global loss exists: there, elements whose gradient is not finite keep their
- * value (every Adam kernel applies that rule) and the rest are updated. */
+ * before the global loss exists: there, elements whose updated second moment would not be
+ * finite (a non-finite gradient, or one whose square overflows) keep p, m, v (every Adam
+ * kernel applies that rule) and the rest are updated. */
 int surrogate_step(mel_ctx* ctx, double* loss_host);
 
 /* Result of an earlier surrogate_step call without draining the stream: `call` is the

@@ -949,7 +949,12 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
   if (r) return r;
   CK(cudaStreamSynchronize(c->stream));
 
-  c->fused_adam = (c->world == 1) && (g->precision == MEL_BF16) && !(g->flags & MEL_FLAG_UNFUSED_ADAM);
+  // the Adam of W_L inside K1 pays off from 4 batch chunks per tile on (DESIGN.md section 7,
+  // measured step at B = 64 / 128 / 192 / 256: unfused 1.88 / 1.95 / 2.06 / 2.09 ms, fused
+  // 2.77 / 2.80 / 3.64 / 1.79 ms): with fewer chunks the staged Adam phase cannot hide behind
+  // the next tile's MMAs, so small batches (the paper's b = 10) run the separate kernel
+  c->fused_adam = (c->world == 1) && (g->precision == MEL_BF16) && !(g->flags & MEL_FLAG_UNFUSED_ADAM) &&
+                  c->B >= 256;
   if (c->world > 1) {
     if (!c->virt) {
       ncclUniqueId id;

@@ -298,10 +298,13 @@ __device__ __forceinline__ void adam4(float4& pp, float4& mm, float4& vv, const 
   float* P = &pp.x; float* Mv = &mm.x; float* V = &vv.x; const float* G = &gg.x;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-    if (!isfinite(G[c])) continue;      // a non-finite gradient element leaves p, m, v as they are
     const float gr = G[c] * scale;
+    const float nv = fmaf(b2, V[c], (1.f - b2) * gr * gr);
+    // an element whose second moment would not be finite (a non-finite gradient, or one whose
+    // square overflows) keeps p, m, v as they are (include/mel.h surrogate_step)
+    if (!isfinite(nv)) continue;
     Mv[c] = fmaf(b1, Mv[c], (1.f - b1) * gr);
-    V[c] = fmaf(b2, V[c], (1.f - b2) * gr * gr);
+    V[c] = nv;
     const float denom = fmaf(__fsqrt_rn(V[c]), inv_sqrt_c2, eps);
     P[c] = fmaf(-step, __fdiv_rn(Mv[c], denom), P[c]);
   }

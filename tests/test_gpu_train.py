@@ -26,9 +26,9 @@ def _bf16_wl(**kw):
 
 
 @pytest.mark.parametrize("n,batch,flags", [(100, 256, 0), (37, 64, 0), (101, 192, 0), (100, 256, 8), (100, 10, 0),
-                                          (37, 100, 0)],
+                                          (37, 100, 0), (37, 300, 0)],
                          ids=["N1e4-B256", "N1369-B64", "N10201-B192", "N1e4-B256-unfusedAdam", "N1e4-B10-paper",
-                              "N1369-B100"])
+                              "N1369-B100", "N1369-B300-fused-padded"])
 def test_bf16_step_reanchored(mel, n, batch, flags):
     """One re-anchored bf16 step at a time: the GPU's output layer runs on
     tcgen05 with bf16 operands (W shadow, H, dY) and fp32 TMEM accumulation.
@@ -79,15 +79,20 @@ def test_bf16_loss_after_1000_steps_free_running(mel):
     assert err <= 2e-2
 
 
-def test_fused_adam_bit_identical_to_unfused(mel):
-    """Adam of W_L inside the output-layer kernel (default, world 1, bf16) reproduces
-    the separate Adam kernel bit for bit (master, moments, shadow) over 40 free-running
-    steps: same arithmetic, only where it runs differs.  N = 10^4 + 37
-    leaves a ragged last tile."""
-    wl = _bf16_wl(n=101, batch=192, capacity=600, threshold=100, sims=40, puts_per_step=40)
+@pytest.mark.parametrize("hidden,batch,overlap", [((256, 256), 256, False), ((64, 64), 320, False),
+                                                  ((256, 256), 256, True)],
+                         ids=["K256-B256", "K64-B320-padded", "K256-B256-overlapped"])
+def test_fused_adam_bit_identical_to_unfused(mel, hidden, batch, overlap, monkeypatch):
+    """Adam of W_L inside the output-layer kernel (default at world 1, bf16, B >= 256)
+    reproduces the separate Adam kernel bit for bit (master, moments, shadow) over 40
+    free-running steps: same arithmetic, only where it runs differs -- in the
+    staged K1 and in the opt-in overlapped K1 (MEL_K1_OVERLAP=1: Adam CTAs fed through the
+    L2 ring).  N = 10^4 + 37 leaves a ragged last tile; B = 320 runs padded to 384."""
+    wl = _bf16_wl(n=101, batch=batch, hidden=hidden, capacity=600, threshold=100, sims=40, puts_per_step=40)
     table = FieldTable(wl)
     states = []
     for flags in (0, mel.FLAG_UNFUSED_ADAM):
+        monkeypatch.setenv("MEL_K1_OVERLAP", "1" if (overlap and flags == 0) else "0")
         ctx = mel.Context(make_config(wl, precision=1, storage=1, flags=flags))
         steps = 0
         for op in design.build_oplog(wl):
@@ -158,7 +163,7 @@ def test_bf16_shapes(mel, hidden, batch):
 
 def test_invalid_configurations_fail_loudly(mel):
     base = dict(n_field=400, hidden=(256, 256), capacity=100, threshold=10, batch=128, precision=1, storage=1)
-    for bad in (dict(threshold=100), dict(batch=0), dict(batch=96), dict(hidden=(256, 100)), dict(storage=0),
+    for bad in (dict(threshold=100), dict(batch=0), dict(hidden=(256, 100)), dict(storage=0),
                 dict(n_field=0)):
         cfg = mel.Config(**{**base, **bad})
         with pytest.raises(mel.MelError) as e:
