@@ -120,6 +120,9 @@ struct OutArgs {
 };
 int out_fwd_f32(const OutArgs& a, cudaStream_t s);   // returns number of partials
 void col_sum(const float* X, int rows, int cols, int ld, float* out, cudaStream_t s);
+// column sums of two matrices with the same row count in one launch (X1 nullable)
+void col_sum2(const float* X0, int cols0, int ld0, float* out0, const float* X1, int cols1, int ld1, float* out1,
+              int rows, cudaStream_t s);
 void reduce_local(StepDev* sd, const double* parts, int n_parts, const ResDev* st, cudaStream_t s);
 void step_finalize(StepDev* sd, double n_field, double lr0, double lr_min, uint64_t halving, double b1, double b2,
                    Mirror* mirror, ResDev* st, cudaStream_t s, uint32_t slot = 0);

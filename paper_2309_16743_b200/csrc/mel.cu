@@ -444,25 +444,32 @@ int head_backward(mel_ctx* c) {
   const int L = c->L;
   Timer t(c, MEL_K_HEAD_BWD, 0);
   uint64_t nl = 0;
-  for (int l = L - 1; l >= 1; --l) {             // weight layer l (1-based), l < L
+  // dZ of every hidden layer first: dZ_{l-1} = (dZ_l W_l) * ReLU'(Z_{l-1}), fused mask (W_l is
+  // only updated by the Adam after the exchange)
+  for (int l = L - 1; l >= 2; --l) {
     const int dout = c->dims[l], din = c->dims[l - 1];
-    const float* dZ = c->d_dz[l - 1];
+    const float* W = c->d_p + c->off[2 * (l - 1)];
+    EpiExtra ex;
+    ex.mask = c->d_z[l - 2];
+    ex.ldm = din;
+    nl += sgemm_auto(false, false, (int)c->B, din, dout, c->d_dz[l - 1], dout, W, din, c->d_dz[l - 2], din,
+                     EPI_RELU_MASK, nullptr, nullptr, 0, c->d_part, c->part_elems, c->stream, ex);
+  }
+  // weight gradients dW_l = dZ_l^T H_{l-1} (K = B; 32 x 32 tiles fill the GPU without split-K)
+  for (int l = L - 1; l >= 1; --l) {
+    const int dout = c->dims[l], din = c->dims[l - 1];
     const float* Hin = (l == 1) ? c->d_xn : c->d_h[l - 2];
     const int ldin = (l == 1) ? 8 : din;
-    float* gW = c->d_g + c->off[2 * (l - 1)];
-    float* gb = c->d_g + c->off[2 * (l - 1) + 1];
-    nl += sgemm_auto(true, false, dout, din, (int)c->B, dZ, dout, Hin, ldin, gW, din, EPI_STORE, nullptr, nullptr, 0,
-                     c->d_part, c->part_elems, c->stream);
-    col_sum(dZ, (int)c->B, dout, dout, gb, c->stream);
+    nl += sgemm_auto(true, false, dout, din, (int)c->B, c->d_dz[l - 1], dout, Hin, ldin, c->d_g + c->off[2 * (l - 1)],
+                     din, EPI_STORE, nullptr, nullptr, 0, c->d_part, c->part_elems, c->stream);
+  }
+  // bias gradients of the hidden layers (column sums over the batch, fp64 accumulation): one launch
+  for (int l = L - 1; l >= 1; l -= 2) {
+    const int l2 = l - 1;
+    col_sum2(c->d_dz[l - 1], c->dims[l], c->dims[l], c->d_g + c->off[2 * (l - 1) + 1],
+             l2 >= 1 ? c->d_dz[l2 - 1] : nullptr, l2 >= 1 ? c->dims[l2] : 0, l2 >= 1 ? c->dims[l2] : 0,
+             l2 >= 1 ? c->d_g + c->off[2 * (l2 - 1) + 1] : nullptr, (int)c->B, c->stream);
     nl += 1;
-    if (l > 1) {
-      const float* W = c->d_p + c->off[2 * (l - 1)];
-      EpiExtra ex;
-      ex.mask = c->d_z[l - 2];                   // dZ_{l-1} = dH_{l-1} * ReLU'(Z_{l-1}), fused
-      ex.ldm = din;
-      nl += sgemm_auto(false, false, (int)c->B, din, dout, dZ, dout, W, din, c->d_dz[l - 2], din, EPI_RELU_MASK,
-                       nullptr, nullptr, 0, c->d_part, c->part_elems, c->stream, ex);
-    }
   }
   c->launches += nl;
   c->klaunch[MEL_K_HEAD_BWD] += nl;
@@ -934,9 +941,13 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
       c->nb = tiles >= 64 ? (e_nb ? atoi(e_nb) : 1) : 1;
       if (c->nb < 1) c->nb = 1;
       if (c->nb > mel_ctx::NBMAX) c->nb = mel_ctx::NBMAX;
+      // bucket boundaries on whole groups of `world` tiles, so every bucket's rows split into
+      // `world` equal parts (tiles is a multiple of world: Npad is padded to 128 x world)
+      const uint32_t groups = tiles / (uint32_t)c->world;
+      if ((uint32_t)c->nb > groups) c->nb = (int)groups;
       for (int j = 0; j < c->nb; ++j) {
-        c->bt0[j] = (uint32_t)((uint64_t)tiles * j / c->nb);
-        c->bt1[j] = (uint32_t)((uint64_t)tiles * (j + 1) / c->nb);
+        c->bt0[j] = (uint32_t)((uint64_t)groups * j / c->nb) * (uint32_t)c->world;
+        c->bt1[j] = (uint32_t)((uint64_t)groups * (j + 1) / c->nb) * (uint32_t)c->world;
       }
     }
     r = tc::prepare(c->tcb, c->Npad, c->B, c->Klast, shadows,

@@ -14,21 +14,24 @@ constexpr int TM = 64, TN = 64, TK = 32;
 // C[M][N] = sum_k A(m,k) B(k,n);  A(m,k) = TA ? A[k*lda+m] : A[m*lda+k];
 // B(k,n) = TB ? B[n*ldb+k] : B[k*ldb+n].  gridDim.z = split-K partitions; with
 // splits > 1, C points at the partial buffer [z][M][ldc].
-template <bool TA, bool TB>
+// T: the CTA's output tile is T x T (64, or 32 for the head's small GEMMs: 4x the CTAs,
+// so they fill the GPU without a split-K pass and its reduction launch)
+template <bool TA, bool TB, int T = 64>
 __global__ void __launch_bounds__(256)
 sgemm_kernel(int M, int N, int K, const float* __restrict__ A, int lda, const float* __restrict__ B, int ldb,
              float* __restrict__ C, int ldc, int epi, const float* __restrict__ bias, float* __restrict__ H, int ldh,
              int k_chunk, EpiExtra ex) {
   pdl_enter();
+  constexpr int TM = T, TN = T, RI = T / 16;
   __shared__ float As[TK][TM + 4];
   __shared__ float Bs[TK][TN + 4];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
   const int kb = blockIdx.z * k_chunk;
   const int ke = min(K, kb + k_chunk);
-  float acc[4][4] = {};
+  float acc[RI][RI] = {};
   for (int k0 = kb; k0 < ke; k0 += TK) {
-    // A tile: 64 x 16
+    // A tile: T x TK
     for (int i = threadIdx.x; i < TM * TK; i += 256) {
       int mm, kk;
       if (TA) { mm = i % TM; kk = i / TM; } else { kk = i % TK; mm = i / TK; }
@@ -48,25 +51,25 @@ sgemm_kernel(int M, int N, int K, const float* __restrict__ A, int lda, const fl
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < TK; ++kk) {
-      float a[4], b[4];
+      float a[RI], b[RI];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+      for (int i = 0; i < RI; ++i) a[i] = As[kk][ty + 16 * i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+      for (int j = 0; j < RI; ++j) b[j] = Bs[kk][tx + 16 * j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < RI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < RI; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
     }
     __syncthreads();
   }
   float* Cz = C + (size_t)blockIdx.z * M * ldc;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < RI; ++i) {
     const int m = m0 + ty + 16 * i;
     if (m >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < RI; ++j) {
       const int n = n0 + tx + 16 * j;
       if (n >= N) continue;
       float v = acc[i][j];
@@ -171,12 +174,25 @@ out_fwd_f32_kernel(OutArgs a) {
 // groups.  Accumulated in fp64 and rounded once, so the result is the fp32 rounding of the
 // (near-)exact sum whatever the order -- closest to the fp64 oracle and insensitive to the
 // grouping (the free-running bf16 trajectory amplifies fp32 order effects)
+// ColSumJob: up to two matrices per launch (the head's bias gradients: one launch for both
+// hidden layers); CTAs [0, ceil(cols0 / 32)) take matrix 0, the rest matrix 1
+struct ColSumJob {
+  const float* X[2];
+  int cols[2], ld[2];
+  float* out[2];
+};
+
 __global__ void __launch_bounds__(1024)
-col_sum_kernel(const float* __restrict__ X, int rows, int cols, int ld, float* __restrict__ out) {
+col_sum_kernel(ColSumJob J, int rows) {
   pdl_enter();
   __shared__ double part[32][33];
+  const int nb0 = (J.cols[0] + 31) / 32;
+  const int w = blockIdx.x < (unsigned)nb0 ? 0 : 1;
+  const float* __restrict__ X = J.X[w];
+  const int cols = J.cols[w], ld = J.ld[w];
+  float* __restrict__ out = J.out[w];
   const int cl = threadIdx.x & 31, grp = threadIdx.x >> 5;
-  const int c = blockIdx.x * 32 + cl;
+  const int c = (blockIdx.x - (w ? nb0 : 0)) * 32 + cl;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   if (c < cols) {
     int r = grp;
@@ -450,7 +466,16 @@ int out_fwd_f32(const OutArgs& a, cudaStream_t s) {
 }
 
 void col_sum(const float* X, int rows, int cols, int ld, float* out, cudaStream_t s) {
-  launch_pdl(col_sum_kernel, dim3((cols + 31) / 32), dim3(1024), 0, s, X, rows, cols, ld, out);
+  col_sum2(X, cols, ld, out, nullptr, 0, 0, nullptr, rows, s);
+}
+
+void col_sum2(const float* X0, int cols0, int ld0, float* out0, const float* X1, int cols1, int ld1, float* out1,
+              int rows, cudaStream_t s) {
+  ColSumJob J;
+  J.X[0] = X0; J.cols[0] = cols0; J.ld[0] = ld0; J.out[0] = out0;
+  J.X[1] = X1; J.cols[1] = X1 ? cols1 : 0; J.ld[1] = ld1; J.out[1] = out1;
+  const int nb = (cols0 + 31) / 32 + (J.cols[1] + 31) / 32;
+  launch_pdl(col_sum_kernel, dim3(nb), dim3(1024), 0, s, J, rows);
 }
 
 // SIMT GEMM that fills the GPU: split-K through `scratch` (>= splits*M*N floats) when
@@ -459,6 +484,18 @@ int sgemm_auto(bool ta, bool tb, int M, int N, int K, const float* A, int lda, c
                int epi, const float* bias, float* H, int ldh, float* scratch, size_t scratch_elems, cudaStream_t s,
                EpiExtra ex) {
   const int tiles = ((M + TM - 1) / TM) * ((N + TN - 1) / TN);
+  if (tiles < 148) {
+    // below one wave of 64 x 64 tiles: 32 x 32 tiles (4x the CTAs), one pass over K, the
+    // epilogue fused -- no partial buffer, no reduction launch (the head's GEMMs at B = 1024:
+    // 256 CTAs for the forward and dH, 64 for dW_2 with its K = B loop)
+    dim3 grid((N + 31) / 32, (M + 31) / 32, 1);
+    const int k_chunk = (K + TK - 1) / TK * TK;
+    if (!ta && !tb) launch_pdl(sgemm_kernel<false, false, 32>, grid, dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk, ex);
+    else if (!ta && tb) launch_pdl(sgemm_kernel<false, true, 32>, grid, dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk, ex);
+    else if (ta && !tb) launch_pdl(sgemm_kernel<true, false, 32>, grid, dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk, ex);
+    else launch_pdl(sgemm_kernel<true, true, 32>, grid, dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk, ex);
+    return 1;
+  }
   int sk = 1;
   while (tiles * sk < 148 && K / (sk * 2) >= 64 && (size_t)(sk * 2) * M * N <= scratch_elems) sk *= 2;
   if (sk == 1) {
