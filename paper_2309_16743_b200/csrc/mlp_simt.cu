@@ -30,25 +30,49 @@ sgemm_kernel(int M, int N, int K, const float* __restrict__ A, int lda, const fl
   const int kb = blockIdx.z * k_chunk;
   const int ke = min(K, kb + k_chunk);
   float acc[RI][RI] = {};
-  for (int k0 = kb; k0 < ke; k0 += TK) {
-    // A tile: T x TK
-    for (int i = threadIdx.x; i < TM * TK; i += 256) {
+  // tile loads double-buffered through registers: tile k0 + TK is fetched from global memory
+  // while tile k0 is multiplied out of SMEM (the head's GEMMs are latency-bound otherwise)
+  constexpr int LA = TM * TK / 256, LB = TN * TK / 256;
+  float ra[LA], rb[LB];
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int u = 0; u < LA; ++u) {
+      const int i = threadIdx.x + 256 * u;
       int mm, kk;
       if (TA) { mm = i % TM; kk = i / TM; } else { kk = i % TK; mm = i / TK; }
       const int gm = m0 + mm, gk = k0 + kk;
-      float v = 0.f;
-      if (gm < M && gk < ke) v = TA ? A[(size_t)gk * lda + gm] : A[(size_t)gm * lda + gk];
-      As[kk][mm] = v;
+      ra[u] = (gm < M && gk < ke) ? (TA ? A[(size_t)gk * lda + gm] : A[(size_t)gm * lda + gk]) : 0.f;
     }
-    for (int i = threadIdx.x; i < TN * TK; i += 256) {
+#pragma unroll
+    for (int u = 0; u < LB; ++u) {
+      const int i = threadIdx.x + 256 * u;
       int nn, kk;
       if (TB) { kk = i % TK; nn = i / TK; } else { nn = i % TN; kk = i / TN; }
       const int gn = n0 + nn, gk = k0 + kk;
-      float v = 0.f;
-      if (gn < N && gk < ke) v = TB ? B[(size_t)gn * ldb + gk] : B[(size_t)gk * ldb + gn];
-      Bs[kk][nn] = v;
+      rb[u] = (gn < N && gk < ke) ? (TB ? B[(size_t)gn * ldb + gk] : B[(size_t)gk * ldb + gn]) : 0.f;
     }
+  };
+  auto stash = [&]() {
+#pragma unroll
+    for (int u = 0; u < LA; ++u) {
+      const int i = threadIdx.x + 256 * u;
+      int mm, kk;
+      if (TA) { mm = i % TM; kk = i / TM; } else { kk = i % TK; mm = i / TK; }
+      As[kk][mm] = ra[u];
+    }
+#pragma unroll
+    for (int u = 0; u < LB; ++u) {
+      const int i = threadIdx.x + 256 * u;
+      int nn, kk;
+      if (TB) { kk = i % TK; nn = i / TK; } else { nn = i % TN; kk = i / TN; }
+      Bs[kk][nn] = rb[u];
+    }
+  };
+  if (kb < ke) fetch(kb);
+  for (int k0 = kb; k0 < ke; k0 += TK) {
+    stash();
     __syncthreads();
+    if (k0 + TK < ke) fetch(k0 + TK);
 #pragma unroll
     for (int kk = 0; kk < TK; ++kk) {
       float a[RI], b[RI];
@@ -484,18 +508,6 @@ int sgemm_auto(bool ta, bool tb, int M, int N, int K, const float* A, int lda, c
                int epi, const float* bias, float* H, int ldh, float* scratch, size_t scratch_elems, cudaStream_t s,
                EpiExtra ex) {
   const int tiles = ((M + TM - 1) / TM) * ((N + TN - 1) / TN);
-  if (tiles < 148) {
-    // below one wave of 64 x 64 tiles: 32 x 32 tiles (4x the CTAs), one pass over K, the
-    // epilogue fused -- no partial buffer, no reduction launch (the head's GEMMs at B = 1024:
-    // 256 CTAs for the forward and dH, 64 for dW_2 with its K = B loop)
-    dim3 grid((N + 31) / 32, (M + 31) / 32, 1);
-    const int k_chunk = (K + TK - 1) / TK * TK;
-    if (!ta && !tb) launch_pdl(sgemm_kernel<false, false, 32>, grid, dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk, ex);
-    else if (!ta && tb) launch_pdl(sgemm_kernel<false, true, 32>, grid, dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk, ex);
-    else if (ta && !tb) launch_pdl(sgemm_kernel<true, false, 32>, grid, dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk, ex);
-    else launch_pdl(sgemm_kernel<true, true, 32>, grid, dim3(256), 0, s, M, N, K, A, lda, B, ldb, C, ldc, epi, bias, H, ldh, k_chunk, ex);
-    return 1;
-  }
   int sk = 1;
   while (tiles * sk < 148 && K / (sk * 2) >= 64 && (size_t)(sk * 2) * M * N <= scratch_elems) sk *= 2;
   if (sk == 1) {
