@@ -315,6 +315,22 @@ int reservoir_stats(mel_ctx* ctx, mel_stats* out);
 int reservoir_dump(mel_ctx* ctx, uint32_t* sim_host, uint32_t* t_host, float* X_host /*C x 5*/,
                    uint32_t* seen_host, uint64_t* put_seq_host, void* payload_host);
 
+/* Checkpoint of the rank's buffer (SPEC's ServerCheckpoint; with mel_get_state /
+ * mel_set_state a full restart point of the step, P:183's fault tolerance): the slots
+ * (payload, metadata, seen counters, put sequence), the counters (population, unseen,
+ * commits q, Philox draws d, evictions, retired-count histogram, FIFO head, FIRO position
+ * list, closed / over) and the puts still pending in the staging ring, so that a context
+ * restored from it draws, evicts and trains exactly as the saved one would have.
+ * reservoir_checkpoint_bytes: size of the blob (synchronises); reservoir_save: writes it to
+ * host memory (synchronises); reservoir_load: restores it into a fresh context created with
+ * the same configuration (n_field, capacity, threshold, batch, storage, policy,
+ * staging_entries, seed) before its first put -- MEL_EINVAL on a mismatch or a malformed
+ * blob, MEL_EPROTO after puts.  The ingest log (mel_ingest.h) is the ingest ring's own
+ * state and is not part of this blob. */
+int reservoir_checkpoint_bytes(mel_ctx* ctx, uint64_t* bytes_host);
+int reservoir_save(mel_ctx* ctx, void* blob_host);
+int reservoir_load(mel_ctx* ctx, const void* blob_host);
+
 /* Validation on a dedicated GPU (validation stalls the consumer):
  * copies src's fp32 parameters (every layer; W_L gathered under ZeRO, collectively) into
  * dst, a context of the same layout on another GPU, over NVLink (cudaMemcpyPeerAsync), and

@@ -1808,6 +1808,119 @@ int reservoir_dump(mel_ctx* c, uint32_t* sim, uint32_t* t, float* X, uint32_t* s
   return MEL_OK;
 }
 
+// ---------------------------------------------------------------------------------
+// Reservoir checkpoint (include/mel.h reservoir_save / reservoir_load)
+// ---------------------------------------------------------------------------------
+namespace {
+struct CkptHdr {
+  char magic[8];                 // "MELRES01"
+  uint32_t C, N, storage, policy, S, theta, batch, pad;
+  uint64_t Npad, seed, tail, drawn, n_pending;
+  uint32_t closed, pad2;
+};
+uint64_t ckpt_bytes(const mel_ctx* c, uint64_t n_pending) {
+  const uint64_t C = c->C, W = (C + 31) / 32, esz = c->cfg.storage == MEL_STORE_F32 ? 4 : 2;
+  return sizeof(CkptHdr) + sizeof(ResDev) + C * (sizeof(SlotMeta) + 4 + 8 + 4 + 4) + 4 * W + C * c->N * esz +
+         n_pending * (sizeof(StMeta) + 4ull * c->N);
+}
+}  // namespace
+
+int reservoir_checkpoint_bytes(mel_ctx* c, uint64_t* bytes) {
+  GUARD(c);
+  if (!bytes) return fail(c, MEL_EINVAL, "null bytes");
+  int r = sync_stream(c);
+  if (r) return r;
+  ResDev st;
+  CK(cudaMemcpy(&st, c->d_st, sizeof st, cudaMemcpyDeviceToHost));
+  *bytes = ckpt_bytes(c, c->tail - st.consumed);
+  return MEL_OK;
+}
+
+int reservoir_save(mel_ctx* c, void* blob) {
+  GUARD(c);
+  if (!blob) return fail(c, MEL_EINVAL, "null blob");
+  int r = sync_stream(c);
+  if (r) return r;
+  CK(cudaStreamSynchronize(c->copy_stream));
+  const uint32_t C = c->C, W = (C + 31) / 32, S = c->cfg.staging_entries;
+  const size_t esz = c->cfg.storage == MEL_STORE_F32 ? 4 : 2;
+  ResDev st;
+  CK(cudaMemcpy(&st, c->d_st, sizeof st, cudaMemcpyDeviceToHost));
+  CkptHdr h{};
+  memcpy(h.magic, "MELRES01", 8);
+  h.C = C; h.N = c->N; h.storage = c->cfg.storage; h.policy = c->cfg.policy; h.S = S;
+  h.theta = c->cfg.threshold; h.batch = c->cfg.batch; h.Npad = c->Npad; h.seed = c->cfg.seed;
+  h.tail = c->tail; h.drawn = c->drawn; h.n_pending = c->tail - st.consumed; h.closed = c->closed ? 1u : 0u;
+  char* o = static_cast<char*>(blob);
+  memcpy(o, &h, sizeof h); o += sizeof h;
+  memcpy(o, &st, sizeof st); o += sizeof st;
+  CK(cudaMemcpy(o, c->ra.meta, sizeof(SlotMeta) * C, cudaMemcpyDeviceToHost)); o += sizeof(SlotMeta) * C;
+  CK(cudaMemcpy(o, c->ra.seen, 4ull * C, cudaMemcpyDeviceToHost)); o += 4ull * C;
+  CK(cudaMemcpy(o, c->ra.put_seq, 8ull * C, cudaMemcpyDeviceToHost)); o += 8ull * C;
+  CK(cudaMemcpy(o, c->ra.bitmap, 4ull * W, cudaMemcpyDeviceToHost)); o += 4ull * W;
+  CK(cudaMemcpy(o, c->ra.pos, 4ull * C, cudaMemcpyDeviceToHost)); o += 4ull * C;
+  CK(cudaMemcpy(o, c->ra.bad, 4ull * C, cudaMemcpyDeviceToHost)); o += 4ull * C;
+  CK(cudaMemcpy2D(o, esz * c->N, c->ra.payload, esz * c->Npad, esz * c->N, C, cudaMemcpyDeviceToHost));
+  o += esz * c->N * C;
+  // the puts still pending in the staging ring: metadata + the fp32 field (from the ring, or
+  // from the caller's buffer for a zero-copy put, which the reservoir_put contract keeps valid)
+  for (uint64_t k = st.consumed; k < c->tail; ++k) {
+    const uint32_t e = (uint32_t)(k % S);
+    memcpy(o, &c->h_stmeta[e], sizeof(StMeta)); o += sizeof(StMeta);
+    const float* src = c->h_stsrc[e] ? c->h_stsrc[e] : c->ra.st_field + (uint64_t)e * c->Npad;
+    CK(cudaMemcpy(o, src, 4ull * c->N, cudaMemcpyDeviceToHost)); o += 4ull * c->N;
+  }
+  return MEL_OK;
+}
+
+int reservoir_load(mel_ctx* c, const void* blob) {
+  GUARD(c);
+  if (!blob) return fail(c, MEL_EINVAL, "null blob");
+  CkptHdr h;
+  const char* i = static_cast<const char*>(blob);
+  memcpy(&h, i, sizeof h); i += sizeof h;
+  if (memcmp(h.magic, "MELRES01", 8) != 0) return fail(c, MEL_EINVAL, "not a reservoir checkpoint");
+  if (h.C != c->C || h.N != c->N || h.storage != c->cfg.storage || h.policy != c->cfg.policy ||
+      h.S != c->cfg.staging_entries || h.theta != c->cfg.threshold || h.batch != c->cfg.batch || h.Npad != c->Npad ||
+      h.seed != c->cfg.seed)
+    return fail(c, MEL_EINVAL, "checkpoint of a different configuration");
+  if (c->tail != 0) return fail(c, MEL_EPROTO, "reservoir_load after puts on this context");
+  if (h.n_pending > c->cfg.staging_entries) return fail(c, MEL_EINVAL, "malformed checkpoint");
+  int r = sync_stream(c);
+  if (r) return r;
+  const uint32_t C = c->C, W = (C + 31) / 32, S = c->cfg.staging_entries;
+  const size_t esz = c->cfg.storage == MEL_STORE_F32 ? 4 : 2;
+  ResDev st;
+  memcpy(&st, i, sizeof st); i += sizeof st;
+  if (h.tail - st.consumed != h.n_pending) return fail(c, MEL_EINVAL, "malformed checkpoint");
+  CK(cudaMemcpy(c->d_st, &st, sizeof st, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->ra.meta, i, sizeof(SlotMeta) * C, cudaMemcpyHostToDevice)); i += sizeof(SlotMeta) * C;
+  CK(cudaMemcpy(c->ra.seen, i, 4ull * C, cudaMemcpyHostToDevice)); i += 4ull * C;
+  CK(cudaMemcpy(c->ra.put_seq, i, 8ull * C, cudaMemcpyHostToDevice)); i += 8ull * C;
+  CK(cudaMemcpy(c->ra.bitmap, i, 4ull * W, cudaMemcpyHostToDevice)); i += 4ull * W;
+  CK(cudaMemcpy(c->ra.pos, i, 4ull * C, cudaMemcpyHostToDevice)); i += 4ull * C;
+  CK(cudaMemcpy(c->ra.bad, i, 4ull * C, cudaMemcpyHostToDevice)); i += 4ull * C;
+  CK(cudaMemcpy2D(c->ra.payload, esz * c->Npad, i, esz * c->N, esz * c->N, C, cudaMemcpyHostToDevice));
+  i += esz * c->N * C;
+  for (uint64_t k = st.consumed; k < h.tail; ++k) {
+    const uint32_t e = (uint32_t)(k % S);
+    memcpy(&c->h_stmeta[e], i, sizeof(StMeta)); i += sizeof(StMeta);
+    c->h_stsrc[e] = nullptr;
+    CK(cudaMemcpy(const_cast<float*>(c->ra.st_field) + (uint64_t)e * c->Npad, i, 4ull * c->N, cudaMemcpyHostToDevice));
+    i += 4ull * c->N;
+  }
+  Mirror& m = *c->h_mirror;
+  m.consumed = st.consumed; m.q = st.q; m.d = st.d; m.evictions = st.evictions;
+  m.p = st.p; m.u = st.u; m.over = st.over; m.n_last = 0;
+  c->tail = h.tail;
+  c->known_consumed = st.consumed;
+  c->drawn = h.drawn;
+  c->closed = h.closed != 0;
+  c->batch_known = false;
+  c->batch_n = 0;
+  return MEL_OK;
+}
+
 int mel_params_copy(mel_ctx* dst, mel_ctx* src) {
   GUARD(src);
   mel_ctx* c = src;                               // errors are reported on (and poison) src

@@ -38,7 +38,8 @@ EXPORTS = ["mel_config_default", "mel_nccl_unique_id", "mel_create", "mel_destro
            "reservoir_stats", "reservoir_dump", "mel_sync", "mel_kernel_time", "mel_kernel_time_reset",
            "mel_launch_count", "mel_set_flags", "mel_debug_counters", "reservoir_ingest",
            "surrogate_train_offline", "reservoir_put_generated", "mel_params_copy", "mel_create_virtual",
-           "surrogate_step_virtual", "mel_stream_wait_event"]
+           "surrogate_step_virtual", "mel_stream_wait_event", "reservoir_checkpoint_bytes", "reservoir_save",
+           "reservoir_load"]
 # include/mel_heat.h (on-device heat-equation client)
 HEAT_EXPORTS = ["mel_heat_create", "mel_heat_basis_bytes", "mel_heat_grid", "mel_heat_tau", "mel_heat_fields",
                 "mel_heat_destroy"]
@@ -184,6 +185,9 @@ def load_library(path: str = LIB_PATH):
         "mel_dataset_close": (None, [vp]),
         "mel_params_copy": (C.c_int, [vp, vp]),
         "mel_stream_wait_event": (C.c_int, [vp, vp]),
+        "reservoir_checkpoint_bytes": (C.c_int, [vp, C.POINTER(u64)]),
+        "reservoir_save": (C.c_int, [vp, vp]),
+        "reservoir_load": (C.c_int, [vp, vp]),
         "mel_create_virtual": (C.c_int, [C.POINTER(_Config), C.c_int, C.c_int, vp, C.POINTER(vp)]),
         "surrogate_step_virtual": (C.c_int, [C.POINTER(vp), C.c_int, C.POINTER(C.c_double)]),
         "reservoir_put_generated": (C.c_int, [vp, vp, C.POINTER(u32), C.POINTER(C.c_float), C.POINTER(u32), u32,
@@ -420,6 +424,18 @@ class Context:
         if d.get("pending", 1) == 0:
             self._zc_refs = []                    # every zero-copy put has been committed
         return d
+
+    def save_reservoir(self) -> np.ndarray:
+        """The buffer's checkpoint blob (include/mel.h reservoir_save)."""
+        n = C.c_uint64()
+        self._check(self.lib.reservoir_checkpoint_bytes(self.h, C.byref(n)))
+        blob = np.empty(n.value, dtype=np.uint8)
+        self._check(self.lib.reservoir_save(self.h, blob.ctypes.data_as(C.c_void_p)))
+        return blob
+
+    def load_reservoir(self, blob: np.ndarray):
+        blob = np.ascontiguousarray(blob, dtype=np.uint8)
+        self._check(self.lib.reservoir_load(self.h, blob.ctypes.data_as(C.c_void_p)))
 
     def dump(self, payload: bool = True) -> dict:
         Cn, N = self.cfg.capacity, self.cfg.n_field
