@@ -143,4 +143,52 @@ int eval_mse_partial(const float* Y, const float* T, int rows, int cols, int ld,
 void eval_inputs(const float* X, const uint32_t* t, int n, uint32_t tau, float lo, float span, float* xn, cudaStream_t s);
 void normalise_fields(const float* src, float* dst, uint64_t n, float lo, float span, cudaStream_t s);
 
+// Fused head of the paper's network (two hidden layers; d0 <= 8 inputs, hidden widths
+// <= 256 and multiples of 32), HEAD_R batch rows per CTA.
+constexpr int HEAD_R = 8;
+// forward in one launch: the batch inputs gathered from the slot metadata (gather_inputs'
+// arithmetic), Z1/H1, Z2/H2 (+ the bf16 copy of H2); with sd set, the last CTA to finish
+// also computes step_prepare's scalars (world 1, fused Adam) once every bad-input flag is in
+struct HeadFwdArgs {
+  ResArgs ra;
+  const int32_t* slots;
+  uint32_t B, tau;
+  const float *W1, *b1, *W2, *b2;
+  int d0, d1, d2;
+  float *xn, *Z1, *H1, *Z2, *H2;
+  __nv_bfloat16* Hb;                    // nullable
+  StepDev* sd;                          // nullable: no fused prepare
+  double n_field, lr0, lr_min, beta1, beta2;
+  uint64_t halving;
+  uint32_t* counter;                    // monotonic CTA-arrival counter (prepare)
+  uint32_t target;                      // its value once every CTA of this launch arrived
+};
+void head_fwd3(const HeadFwdArgs& a, cudaStream_t s);
+// backward in two launches, given dZ2 (ReLU' applied).  head_bwd3_kernel: row CTAs compute
+// dZ1 = (dZ2 W2) . ReLU'(Z1) for HEAD_R rows and their partial dW1 / db1 sums; dW2 CTAs the
+// partial dW2 = dZ2^T H1 (+ db2, fp64) of a 64-row batch slice.  head_fin3_kernel: the
+// fixed-order reductions into the gradient (deterministic); with sd set (world 1) it also
+// folds K1's SSE partials and runs step_finalize's scalars.
+struct HeadBwdArgs {
+  const float *dz2, *W2, *z1, *h1, *xn;
+  int B, d0, d1, d2;
+  float *gW1, *gb1, *gW2, *gb2;
+  float* p_dw1;                         // [row CTAs][d1][8]
+  double* p_db1;                        // [row CTAs][d1]
+  float* p_dw2;                         // [slices][d2][d1]
+  double* p_db2;                        // [slices][d2]
+  // fused reduce_local + step_finalize (world 1); sd == nullptr: off
+  StepDev* sd;
+  const double* sse_parts;
+  int n_sse_parts;
+  ResDev* st;
+  Mirror* mirror;
+  uint32_t slot;
+  double n_field, lr0, lr_min, beta1, beta2;
+  uint64_t halving;
+};
+__host__ __device__ inline int head_bwd3_row_ctas(int B) { return (B + HEAD_R - 1) / HEAD_R; }
+void head_bwd3(const HeadBwdArgs& a, cudaStream_t s);
+size_t head_dw2_part_elems(int B, int d1, int d2);
+
 }  // namespace mel

@@ -112,6 +112,16 @@ struct mel_ctx {
   float* d_h[2] = {nullptr, nullptr};
   float* d_dz[2] = {nullptr, nullptr};
   float* d_dy = nullptr;           // fp32 mode [B][Npad]
+  // fused head (two hidden layers): one forward and one backward launch per step
+  bool head_fused = false;
+  bool prep_fused = false;         // this step's step_prepare ran inside the head forward
+  int last_nparts = 0;             // K1's SSE partials of this step
+  uint32_t* d_hcnt = nullptr;      // monotonic CTA-arrival counter of the head forward
+  uint32_t hf_n = 0;               // head-forward launches with the fused prepare so far
+  float* d_hp_dw1 = nullptr;       // [row CTAs][d1][8] partial dW1
+  double* d_hp_db1 = nullptr;      // [row CTAs][d1] partial db1
+  float* d_hp_dw2 = nullptr;       // [64-row slices][d2][d1] partial dW2
+  double* d_hp_db2 = nullptr;      // [64-row slices][d2] partial db2
   float* d_part = nullptr;         // split-K partials
   size_t part_elems = 0;
   double* d_sse_part = nullptr;
@@ -440,10 +450,34 @@ int gather_master(mel_ctx* c, bool moments) {
 
 // backward of the head layers given dZ of the last hidden layer (d_dz[L-2]); every
 // GEMM is split-K through the partial buffer when its grid is below one wave
+// world 1 with the fused head: reduce_local and step_finalize run inside the head backward's
+// reduction launch (nothing is exchanged between them and the step's scalars)
+inline bool fin_fused(const mel_ctx* c) { return c->head_fused && c->world == 1 && !c->virt; }
+
 int head_backward(mel_ctx* c) {
   const int L = c->L;
   Timer t(c, MEL_K_HEAD_BWD, 0);
   uint64_t nl = 0;
+  if (c->head_fused) {
+    HeadBwdArgs a;
+    a.dz2 = c->d_dz[1]; a.W2 = c->d_p + c->off[2]; a.z1 = c->d_z[0]; a.h1 = c->d_h[0]; a.xn = c->d_xn;
+    a.B = (int)c->B; a.d0 = (int)c->dims[0]; a.d1 = (int)c->dims[1]; a.d2 = (int)c->dims[2];
+    a.gW1 = c->d_g + c->off[0]; a.gb1 = c->d_g + c->off[1]; a.gW2 = c->d_g + c->off[2]; a.gb2 = c->d_g + c->off[3];
+    a.p_dw1 = c->d_hp_dw1; a.p_db1 = c->d_hp_db1; a.p_dw2 = c->d_hp_dw2; a.p_db2 = c->d_hp_db2;
+    a.sd = nullptr;
+    if (fin_fused(c)) {
+      // world 1: nothing is exchanged before the step's scalars, so K1's SSE partials and
+      // step_finalize fold into the gradient reduction's launch
+      a.sd = c->d_sd; a.sse_parts = c->d_sse_part; a.n_sse_parts = c->last_nparts; a.st = c->d_st;
+      a.mirror = c->d_mirror; a.slot = (uint32_t)(c->calls % MEL_RESULT_RING);
+      a.n_field = (double)c->N; a.lr0 = c->cfg.lr0; a.lr_min = c->cfg.lr_min; a.halving = c->cfg.lr_halving_samples;
+      a.beta1 = c->cfg.beta1; a.beta2 = c->cfg.beta2;
+    }
+    head_bwd3(a, c->stream);
+    c->launches += 2;
+    c->klaunch[MEL_K_HEAD_BWD] += 2;
+    return check_launch(c, "head backward");
+  }
   // dZ of every hidden layer first: dZ_{l-1} = (dZ_l W_l) * ReLU'(Z_{l-1}), fused mask (W_l is
   // only updated by the Adam after the exchange)
   for (int l = L - 1; l >= 2; --l) {
@@ -526,7 +560,8 @@ int train_step_fp32(mel_ctx* c) {
   }
   int r = check_launch(c, "output layer fp32");
   if (r) return r;
-  reduce_local(c->d_sd, c->d_sse_part, nparts, c->d_st, c->stream);
+  c->last_nparts = nparts;
+  if (!fin_fused(c)) reduce_local(c->d_sd, c->d_sse_part, nparts, c->d_st, c->stream);
   return MEL_OK;
 }
 
@@ -581,7 +616,8 @@ int bf16_post_k1(mel_ctx* c, const tc::OutTcArgs& a, int nparts) {
   }
   int r = check_launch(c, "output layer tcgen05");
   if (r) return r;
-  reduce_local(c->d_sd, c->d_sse_part, nparts, c->d_st, c->stream);
+  c->last_nparts = nparts;
+  if (!fin_fused(c)) reduce_local(c->d_sd, c->d_sse_part, nparts, c->d_st, c->stream);
   return MEL_OK;
 }
 
@@ -597,7 +633,7 @@ int train_step_bf16(mel_ctx* c) {
       stage_count(c->d_sd, c->d_st, c->stream);
       NK(ncclAllReduce(&c->d_sd->n_glob, &c->d_sd->n_glob, 1, ncclFloat64, ncclSum, c->comm, c->stream));
     }
-    bf16_prepare(c);
+    if (!c->prep_fused) bf16_prepare(c);
   }
   int nparts = 0;
   if (!c->zero || c->peer) {
@@ -632,6 +668,28 @@ int step_front(mel_ctx* c) {
     CK(cudaMemsetAsync(&c->d_st->n_last, 0, 4, c->stream));
     c->batch_n = 0;
   }
+  c->prep_fused = false;
+  if (c->head_fused) {
+    // gather + both hidden layers (+ the step scalars of the fused Adam, world 1) in one launch
+    Timer t(c, MEL_K_HEAD_FWD, 1);
+    HeadFwdArgs a;
+    memset(&a, 0, sizeof a);
+    a.ra = c->ra; a.slots = c->d_slots; a.B = c->B; a.tau = c->cfg.steps_per_sim;
+    a.W1 = c->d_p + c->off[0]; a.b1 = c->d_p + c->off[1]; a.W2 = c->d_p + c->off[2]; a.b2 = c->d_p + c->off[3];
+    a.d0 = (int)c->dims[0]; a.d1 = (int)c->dims[1]; a.d2 = (int)c->dims[2];
+    a.xn = c->d_xn; a.Z1 = c->d_z[0]; a.H1 = c->d_h[0]; a.Z2 = c->d_z[1]; a.H2 = c->d_h[1];
+    a.Hb = c->cfg.precision == MEL_BF16 ? c->tcb.h_bf16 : nullptr;
+    if (c->cfg.precision == MEL_BF16 && c->fused_adam && !c->peer) {
+      a.sd = c->d_sd; a.n_field = (double)c->N; a.lr0 = c->cfg.lr0; a.lr_min = c->cfg.lr_min;
+      a.halving = c->cfg.lr_halving_samples; a.beta1 = c->cfg.beta1; a.beta2 = c->cfg.beta2;
+      a.counter = c->d_hcnt;
+      a.target = (c->hf_n + 1) * ((c->B + HEAD_R - 1) / HEAD_R);
+      c->hf_n += 1;
+      c->prep_fused = true;
+    }
+    head_fwd3(a, c->stream);
+    return check_launch(c, "head forward");
+  }
   {
     Timer t(c, MEL_K_GATHER, 1);
     launch_gather(c->ra, c->d_slots, c->B, c->cfg.steps_per_sim, c->d_xn, c->stream);
@@ -650,7 +708,7 @@ int step_front(mel_ctx* c) {
 // fuse), the shadow flip, the result record for surrogate_step_result
 int step_finish(mel_ctx* c) {
   int r;
-  {
+  if (!fin_fused(c)) {
     Timer t(c, MEL_K_LOSS, 1);
     step_finalize(c->d_sd, (double)c->N, c->cfg.lr0, c->cfg.lr_min, c->cfg.lr_halving_samples, c->cfg.beta1,
                   c->cfg.beta2, c->d_mirror, c->d_st, c->stream, (uint32_t)(c->calls % MEL_RESULT_RING));
@@ -911,6 +969,20 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
   }
   DALLOC(c->d_sd, 1);
   CK(cudaMemset(c->d_sd, 0, sizeof(StepDev)));
+  {
+    const char* hf = getenv("MEL_HEAD_FUSED");
+    c->head_fused = (!hf || atoi(hf) != 0) && c->L == 3 && c->dims[0] <= 8 && c->dims[1] % 32 == 0 &&
+                    c->dims[2] % 32 == 0 && c->dims[1] <= 256 && c->dims[2] <= 256;
+    if (c->head_fused) {
+      const int nrow = head_bwd3_row_ctas((int)c->B);
+      DALLOC(c->d_hcnt, 1);
+      CK(cudaMemset(c->d_hcnt, 0, 4));
+      DALLOC(c->d_hp_dw1, (size_t)nrow * c->dims[1] * 8);
+      DALLOC(c->d_hp_db1, (size_t)nrow * c->dims[1]);
+      DALLOC(c->d_hp_dw2, head_dw2_part_elems((int)c->B, (int)c->dims[1], (int)c->dims[2]));
+      DALLOC(c->d_hp_db2, head_dw2_part_elems((int)c->B, 1, (int)c->dims[2]));
+    }
+  }
   if (g->precision == MEL_FP32) {
     DALLOC(c->d_dy, (size_t)c->B * c->Npad);
     const int sp = splits_for(c->Npad);

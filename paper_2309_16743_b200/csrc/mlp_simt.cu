@@ -259,9 +259,9 @@ __global__ void splitk_reduce_epi_kernel(int M, int N, int splits, const float* 
   }
 }
 
-__global__ void reduce_local_kernel(StepDev* sd, const double* parts, int n_parts, const ResDev* st) {
-  pdl_enter();
-  __shared__ double s[256];
+// [SSE, n] of this rank's step from K1's per-CTA SSE partials (256 threads, fixed order)
+__device__ __forceinline__ void reduce_local_block(StepDev* sd, const double* parts, int n_parts, const ResDev* st,
+                                                   double* s) {
   double v = 0.0;
   for (int i = threadIdx.x; i < n_parts; i += 256) v += parts[i];
   s[threadIdx.x] = v;
@@ -274,9 +274,14 @@ __global__ void reduce_local_kernel(StepDev* sd, const double* parts, int n_part
   if (threadIdx.x == 0) { sd->red[0] = s[0]; sd->red[1] = st->bad_batch ? nan("") : (double)st->n_last; }
 }
 
-__global__ void step_finalize_kernel(StepDev* sd, double n_field, double lr0, double lr_min, uint64_t halving,
-                                     double b1, double b2, Mirror* mirror, ResDev* st, uint32_t slot) {
+__global__ void reduce_local_kernel(StepDev* sd, const double* parts, int n_parts, const ResDev* st) {
   pdl_enter();
+  __shared__ double s[256];
+  reduce_local_block(sd, parts, n_parts, st, s);
+}
+
+__device__ void finalize_scalars(StepDev* sd, double n_field, double lr0, double lr_min, uint64_t halving, double b1,
+                                 double b2, Mirror* mirror, ResDev* st, uint32_t slot) {
   const double sse = sd->red[0], n = sd->red[1];
   st->n_last = 0;                       // a batch is consumed by exactly one step
   st->bad_batch = 0;
@@ -314,12 +319,19 @@ __global__ void step_finalize_kernel(StepDev* sd, double n_field, double lr0, do
   mirror->adam_k = k; mirror->samples = sd->S;
 }
 
+__global__ void step_finalize_kernel(StepDev* sd, double n_field, double lr0, double lr_min, uint64_t halving,
+                                     double b1, double b2, Mirror* mirror, ResDev* st, uint32_t slot) {
+  pdl_enter();
+  finalize_scalars(sd, n_field, lr0, lr_min, halving, b1, b2, mirror, st, slot);
+}
+
 // Step scalars ahead of the output-layer kernel (world == 1, fused Adam): the same
 // values step_finalize computes afterwards (scale, lr, bias corrections of step k+1).
-__global__ void step_prepare_kernel(StepDev* sd, const ResDev* st, double n_field, double lr0, double lr_min,
-                                    uint64_t halving, double b1, double b2, int global_n) {
-  pdl_enter();
-  const double n = global_n ? sd->n_glob : (st->bad_batch ? nan("") : (double)st->n_last);
+// the step's scalars ahead of K1 (the fused Adam needs lr, bias corrections, the gradient scale)
+__device__ __forceinline__ void prepare_scalars(StepDev* sd, const ResDev* st, double n_field, double lr0,
+                                                double lr_min, uint64_t halving, double b1, double b2, int global_n) {
+  const uint32_t bad = *(volatile const uint32_t*)&st->bad_batch;
+  const double n = global_n ? sd->n_glob : (bad ? nan("") : (double)st->n_last);
   if (!(n > 0.0)) { sd->skip = 1; return; }            // no samples, or non-finite inputs (NaN)
   sd->skip = 0;
   sd->scale = (float)(1.0 / (n_field * n));
@@ -327,6 +339,12 @@ __global__ void step_prepare_kernel(StepDev* sd, const ResDev* st, double n_fiel
   const uint64_t k = sd->k + 1;
   sd->c1 = (float)(1.0 - pow(b1, (double)k));
   sd->c2 = (float)(1.0 - pow(b2, (double)k));
+}
+
+__global__ void step_prepare_kernel(StepDev* sd, const ResDev* st, double n_field, double lr0, double lr_min,
+                                    uint64_t halving, double b1, double b2, int global_n) {
+  pdl_enter();
+  prepare_scalars(sd, st, n_field, lr0, lr_min, halving, b1, b2, global_n);
 }
 
 // Adam (bias-corrected), flat over every tensor; g is the raw dS/dtheta and is
@@ -518,6 +536,296 @@ int sgemm_auto(bool ta, bool tb, int M, int N, int K, const float* A, int lda, c
   launch_pdl(splitk_reduce_epi_kernel, dim3(grid_for((uint64_t)M * N)), dim3(256), 0, s, M, N, sk, scratch, C, ldc, epi, bias, H, ldh, ex);
   return 2;
 }
+
+// ---- fused head (paper shape: 6 -> 256 -> 256) --------------------------------
+// Forward: every output is accumulated k ascending from 0, then + bias (the generic sgemm's
+// order without its split-K).  Backward: phase 1 (head_bwd3) writes per-block partial sums,
+// phase 2 (head_fin3) reduces them in a fixed order -- deterministic, no atomics on data.
+constexpr int HKC = 32;          // W2 columns per SMEM chunk (forward)
+constexpr int HWP = HKC + 4;     // its row pitch (float4 reads conflict-free)
+constexpr int HSL = 64;          // batch rows per dW2 slice (backward)
+constexpr int HJT = 16;          // W2 rows per dW2 CTA (backward)
+
+__global__ void __launch_bounds__(256) head_fwd3_kernel(HeadFwdArgs a) {
+  pdl_enter();
+  __shared__ float xs[HEAD_R][8];
+  __shared__ __align__(16) float h1s[HEAD_R][256];
+  __shared__ __align__(16) float ws[256 * HWP];
+  const int tid = threadIdx.x;
+  const uint32_t b0 = blockIdx.x * HEAD_R;
+  // the batch's normalised inputs (reading Q13), gather_inputs' arithmetic
+  if (tid < HEAD_R) {
+    const uint32_t b = b0 + tid;
+    float out[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (b < a.B) {
+      const uint32_t n = a.ra.st->n_last;
+      if (b < n) {
+        if (a.ra.bad[a.slots[b]]) atomicOr(&a.ra.st->bad_batch, 1u);     // reset by step_finalize
+        const SlotMeta m = a.ra.meta[a.slots[b]];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) out[c] = normalise_rn(m.X[c], a.ra.lo, a.ra.span);
+        out[5] = __fdiv_rn((float)m.t, (float)a.tau);
+      }
+      float4* dst = reinterpret_cast<float4*>(a.xn + (uint64_t)b * 8);
+      dst[0] = make_float4(out[0], out[1], out[2], out[3]);
+      dst[1] = make_float4(out[4], out[5], out[6], out[7]);
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) xs[tid][c] = out[c];
+  }
+  // W2 [d2][d1] streams through SMEM in HKC-column chunks; the next chunk is fetched into
+  // registers while this one is multiplied
+  constexpr int PER = HKC / 4;   // float4 per thread per chunk (256 rows x HKC columns)
+  float4 pre[PER];
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int f = tid + 256 * u, jj = f / (HKC / 4), c4 = f % (HKC / 4);
+      pre[u] = jj < a.d2 ? *reinterpret_cast<const float4*>(a.W2 + (uint64_t)jj * a.d1 + k0 + 4 * c4)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  fetch(0);
+  __syncthreads();
+  const int nr = (int)min((uint32_t)HEAD_R, a.B > b0 ? a.B - b0 : 0u);
+  // layer 1: thread j -> unit j
+  if (tid < a.d1) {
+    float w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = i < a.d0 ? a.W1[tid * a.d0 + i] : 0.f;
+    const float bj = a.b1[tid];
+#pragma unroll
+    for (int r = 0; r < HEAD_R; ++r) {
+      float acc = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (i < a.d0) acc = fmaf(xs[r][i], w[i], acc);
+      const float z = acc + bj, h = fmaxf(z, 0.f);
+      h1s[r][tid] = h;
+      if (r < nr) {
+        const uint64_t o = (uint64_t)(b0 + r) * a.d1 + tid;
+        a.Z1[o] = z;
+        a.H1[o] = h;
+      }
+    }
+  }
+  // layer 2: thread j -> unit j, HEAD_R rows
+  float acc[HEAD_R];
+#pragma unroll
+  for (int r = 0; r < HEAD_R; ++r) acc[r] = 0.f;
+  for (int k0 = 0; k0 < a.d1; k0 += HKC) {
+    __syncthreads();                                   // previous chunk consumed (h1s complete)
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int f = tid + 256 * u, jj = f / (HKC / 4), c4 = f % (HKC / 4);
+      *reinterpret_cast<float4*>(&ws[jj * HWP + 4 * c4]) = pre[u];
+    }
+    __syncthreads();
+    if (k0 + HKC < a.d1) fetch(k0 + HKC);
+#pragma unroll
+    for (int kk = 0; kk < HKC; kk += 4) {
+      const float4 w = *reinterpret_cast<const float4*>(&ws[tid * HWP + kk]);
+#pragma unroll
+      for (int r = 0; r < HEAD_R; ++r) {
+        const float4 h = *reinterpret_cast<const float4*>(&h1s[r][k0 + kk]);
+        acc[r] = fmaf(h.x, w.x, acc[r]);
+        acc[r] = fmaf(h.y, w.y, acc[r]);
+        acc[r] = fmaf(h.z, w.z, acc[r]);
+        acc[r] = fmaf(h.w, w.w, acc[r]);
+      }
+    }
+  }
+  if (tid < a.d2) {
+    const float bj = a.b2[tid];
+    for (int r = 0; r < nr; ++r) {
+      const uint64_t o = (uint64_t)(b0 + r) * a.d2 + tid;
+      const float z = acc[r] + bj, h = fmaxf(z, 0.f);
+      a.Z2[o] = z;
+      a.H2[o] = h;
+      if (a.Hb) a.Hb[o] = __float2bfloat16_rn(h);
+    }
+  }
+  if (a.sd) {
+    // fused step_prepare: the last CTA to arrive sees every CTA's bad-input flag
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      if (atomicAdd(a.counter, 1u) == a.target - 1u) {
+        __threadfence();
+        prepare_scalars(a.sd, a.ra.st, a.n_field, a.lr0, a.lr_min, a.halving, a.beta1, a.beta2, 0);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) head_bwd3_kernel(HeadBwdArgs a) {
+  pdl_enter();
+  __shared__ __align__(16) float sm[HEAD_R * 256 + HEAD_R * 8];
+  const int tid = threadIdx.x;
+  const int n_row = head_bwd3_row_ctas(a.B);
+  if ((int)blockIdx.x < n_row) {
+    // ===== row CTA: dZ1 = (dZ2 W2) . ReLU'(Z1) for HEAD_R rows; partial dW1 / db1 =====
+    float* dz = sm;                                    // [HEAD_R][256]
+    float* xs = sm + HEAD_R * 256;                     // [HEAD_R][8]
+    const int b0 = blockIdx.x * HEAD_R;
+    const int nr = min(HEAD_R, a.B - b0);
+    for (int i = tid; i < HEAD_R * 256; i += 256) {
+      const int r = i / 256, j = i % 256;
+      dz[i] = (r < nr && j < a.d2) ? a.dz2[(uint64_t)(b0 + r) * a.d2 + j] : 0.f;
+    }
+    if (tid < HEAD_R * 8) {
+      const int r = tid / 8, i = tid % 8;
+      xs[tid] = r < nr ? a.xn[(uint64_t)(b0 + r) * 8 + i] : 0.f;
+    }
+    const int k = tid < a.d1 ? tid : 0;
+    // W2 column k in 16-row chunks through registers (coalesced across k), one chunk ahead
+    float wn[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) wn[u] = u < a.d2 ? a.W2[(uint64_t)u * a.d1 + k] : 0.f;
+    __syncthreads();
+    float acc[HEAD_R];
+#pragma unroll
+    for (int r = 0; r < HEAD_R; ++r) acc[r] = 0.f;
+    for (int j0 = 0; j0 < a.d2; j0 += 16) {
+      float w[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) w[u] = wn[u];
+      if (j0 + 16 < a.d2) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) wn[u] = a.W2[(uint64_t)(j0 + 16 + u) * a.d1 + k];
+      }
+#pragma unroll
+      for (int u = 0; u < 16; u += 4) {
+#pragma unroll
+        for (int r = 0; r < HEAD_R; ++r) {
+          const float4 d = *reinterpret_cast<const float4*>(&dz[r * 256 + j0 + u]);
+          acc[r] = fmaf(d.x, w[u], acc[r]);
+          acc[r] = fmaf(d.y, w[u + 1], acc[r]);
+          acc[r] = fmaf(d.z, w[u + 2], acc[r]);
+          acc[r] = fmaf(d.w, w[u + 3], acc[r]);
+        }
+      }
+    }
+    if (tid < a.d1) {
+      float pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      double pdb = 0.0;
+#pragma unroll
+      for (int r = 0; r < HEAD_R; ++r) {
+        if (r >= nr) break;
+        const float d = a.z1[(uint64_t)(b0 + r) * a.d1 + k] > 0.f ? acc[r] : 0.f;   // ReLU'(0) = 0 (R20)
+        pdb += (double)d;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) pw[i] = fmaf(d, xs[r * 8 + i], pw[i]);
+      }
+      float4* dst = reinterpret_cast<float4*>(a.p_dw1 + ((uint64_t)blockIdx.x * a.d1 + k) * 8);
+      dst[0] = make_float4(pw[0], pw[1], pw[2], pw[3]);
+      dst[1] = make_float4(pw[4], pw[5], pw[6], pw[7]);
+      a.p_db1[(uint64_t)blockIdx.x * a.d1 + k] = pdb;
+    }
+    return;
+  }
+  // ===== dW2 CTA: slice sl (HSL batch rows) x W2 rows [HJT jt, HJT jt + HJT): partial
+  // dW2[j][k] = sum_b dZ2[b][j] H1[b][k] (thread k), partial db2 (fp64) =====
+  const int w = blockIdx.x - n_row;
+  const int njt = a.d2 / HJT;
+  const int sl = w / njt, jt = w % njt;
+  const int bs = sl * HSL, be = min(a.B, bs + HSL);
+  float* dzs = sm;                                      // [HSL][HJT]
+  for (int i = tid; i < HSL * HJT; i += 256) {
+    const int r = i / HJT, j = i % HJT, b = bs + r;
+    dzs[i] = b < be ? a.dz2[(uint64_t)b * a.d2 + jt * HJT + j] : 0.f;
+  }
+  const int k = tid < a.d1 ? tid : 0;
+  float hn[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) hn[u] = bs + u < be ? a.h1[(uint64_t)(bs + u) * a.d1 + k] : 0.f;
+  __syncthreads();
+  float acc[HJT];
+#pragma unroll
+  for (int j = 0; j < HJT; ++j) acc[j] = 0.f;
+  for (int r0 = 0; r0 < HSL; r0 += 8) {
+    float h[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) h[u] = hn[u];
+    if (r0 + 8 < HSL) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int b = bs + r0 + 8 + u;
+        hn[u] = b < be ? a.h1[(uint64_t)b * a.d1 + k] : 0.f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+#pragma unroll
+      for (int j = 0; j < HJT; j += 4) {
+        const float4 d = *reinterpret_cast<const float4*>(&dzs[(r0 + u) * HJT + j]);
+        acc[j] = fmaf(d.x, h[u], acc[j]);
+        acc[j + 1] = fmaf(d.y, h[u], acc[j + 1]);
+        acc[j + 2] = fmaf(d.z, h[u], acc[j + 2]);
+        acc[j + 3] = fmaf(d.w, h[u], acc[j + 3]);
+      }
+    }
+  }
+  if (tid < a.d1) {
+#pragma unroll
+    for (int j = 0; j < HJT; ++j) a.p_dw2[((uint64_t)sl * a.d2 + jt * HJT + j) * a.d1 + k] = acc[j];
+  }
+  if (tid < HJT) {
+    double t = 0.0;
+    for (int r = 0; r < HSL; ++r) t += (double)dzs[r * HJT + tid];
+    a.p_db2[(uint64_t)sl * a.d2 + jt * HJT + tid] = t;
+  }
+}
+
+// phase 2: the fixed-order reductions of the head's partial gradients (one output per
+// thread); with sd set (world 1) block 0 then also folds K1's SSE partials into [SSE, n]
+// and runs step_finalize's scalars (the step's last small kernels in one launch)
+__global__ void __launch_bounds__(256) head_fin3_kernel(HeadBwdArgs a) {
+  pdl_enter();
+  __shared__ double sred[256];
+  const int n_row = head_bwd3_row_ctas(a.B), n_sl = (a.B + HSL - 1) / HSL;
+  const int n_w2 = a.d2 * a.d1, n_w1 = a.d1 * a.d0;
+  const int o = blockIdx.x * 256 + threadIdx.x;
+  if (o < n_w2) {
+    float t = 0.f;
+    for (int c = 0; c < n_sl; ++c) t += a.p_dw2[(uint64_t)c * n_w2 + o];
+    a.gW2[o] = t;
+  } else if (o < n_w2 + n_w1) {
+    const int q = o - n_w2, k = q / a.d0, i = q % a.d0;
+    float t = 0.f;
+    for (int c = 0; c < n_row; ++c) t += a.p_dw1[((uint64_t)c * a.d1 + k) * 8 + i];
+    a.gW1[q] = t;
+  } else if (o < n_w2 + n_w1 + a.d1) {
+    const int k = o - n_w2 - n_w1;
+    double t = 0.0;
+    for (int c = 0; c < n_row; ++c) t += a.p_db1[(uint64_t)c * a.d1 + k];
+    a.gb1[k] = (float)t;
+  } else if (o < n_w2 + n_w1 + a.d1 + a.d2) {
+    const int j = o - n_w2 - n_w1 - a.d1;
+    double t = 0.0;
+    for (int c = 0; c < n_sl; ++c) t += a.p_db2[(uint64_t)c * a.d2 + j];
+    a.gb2[j] = (float)t;
+  }
+  if (a.sd && blockIdx.x == 0) {
+    reduce_local_block(a.sd, a.sse_parts, a.n_sse_parts, a.st, sred);
+    __syncthreads();
+    if (threadIdx.x == 0)
+      finalize_scalars(a.sd, a.n_field, a.lr0, a.lr_min, a.halving, a.beta1, a.beta2, a.mirror, a.st, a.slot);
+  }
+}
+
+void head_fwd3(const HeadFwdArgs& a, cudaStream_t s) {
+  launch_pdl(head_fwd3_kernel, dim3((a.B + HEAD_R - 1) / HEAD_R), dim3(256), 0, s, a);
+}
+
+void head_bwd3(const HeadBwdArgs& a, cudaStream_t s) {
+  const int n = head_bwd3_row_ctas(a.B) + ((a.B + HSL - 1) / HSL) * (a.d2 / HJT);
+  launch_pdl(head_bwd3_kernel, dim3(n), dim3(256), 0, s, a);
+  const int n_out = a.d2 * a.d1 + a.d1 * a.d0 + a.d1 + a.d2;
+  launch_pdl(head_fin3_kernel, dim3((n_out + 255) / 256), dim3(256), 0, s, a);
+}
+
+size_t head_dw2_part_elems(int B, int d1, int d2) { return (size_t)((B + HSL - 1) / HSL) * d1 * d2; }
 
 void reduce_local(StepDev* sd, const double* parts, int n_parts, const ResDev* st, cudaStream_t s) {
   launch_pdl(reduce_local_kernel, dim3(1), dim3(256), 0, s, sd, parts, n_parts, st);

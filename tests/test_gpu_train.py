@@ -80,8 +80,8 @@ def test_bf16_loss_after_1000_steps_free_running(mel):
 
 
 @pytest.mark.parametrize("hidden,batch,overlap", [((256, 256), 256, False), ((64, 64), 320, False),
-                                                  ((256, 256), 256, True)],
-                         ids=["K256-B256", "K64-B320-padded", "K256-B256-overlapped"])
+                                                  ((256, 256), 256, True), ((64, 64), 320, True)],
+                         ids=["K256-B256", "K64-B320-padded", "K256-B256-overlapped", "K64-B320-overlapped"])
 def test_fused_adam_bit_identical_to_unfused(mel, hidden, batch, overlap, monkeypatch):
     """Adam of W_L inside the output-layer kernel (default at world 1, bf16, B >= 256)
     reproduces the separate Adam kernel bit for bit (master, moments, shadow) over 40
@@ -202,3 +202,40 @@ def test_step_result_matches_synchronous_loss(mel):
         b.step_result(calls - 17)
     with pytest.raises(mel.MelError):
         b.step_result(calls)
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_fused_head_matches_generic_head(mel, precision, monkeypatch):
+    """The fused head kernels (forward: one launch for the gather, both hidden layers and the
+    step scalars; backward: per-block partials + one fixed-order reduction launch that also
+    finalises the step at world 1) against the generic per-GEMM head path (MEL_HEAD_FUSED=0,
+    split-K SGEMMs, separate gather / prepare / reduce / finalize kernels) over 30
+    free-running steps: the sums are grouped differently, so losses and parameters agree to
+    fp32 rounding."""
+    wl = _bf16_wl(n=37, batch=320, hidden=(256, 256), capacity=600, threshold=100, sims=40, puts_per_step=40)
+    table = FieldTable(wl)
+    states, losses = [], []
+    for fused in ("1", "0"):
+        monkeypatch.setenv("MEL_HEAD_FUSED", fused)
+        ctx = mel.Context(make_config(wl, precision=precision, storage=precision))
+        steps, ls = 0, []
+        for op in design.build_oplog(wl):
+            if op[0] == "PUT":
+                _, r, s, t = op
+                ctx.put(s, t, table.Xs(s), table.field(s, t))
+            elif op[0] == "SAMPLE":
+                ctx.sample()
+            elif op[0] == "STEP":
+                rc, lo = ctx.step(want_loss=True)
+                if rc == 0:
+                    steps += 1
+                    ls.append(lo)
+                    if steps == 30:
+                        break
+        assert steps == 30
+        states.append(ctx.get_state())
+        losses.append(np.array(ls))
+    assert abs(losses[0][0] - losses[1][0]) <= 1e-6 * losses[1][0]   # first step: forward only
+    assert np.max(np.abs(losses[0] - losses[1]) / losses[1]) <= 1e-4
+    for x, y in zip(states[0]["p"], states[1]["p"]):
+        assert rel_norm(x, y) <= (1e-5 if precision == 0 else 1e-3)   # bf16: H2 rounding flips compound
