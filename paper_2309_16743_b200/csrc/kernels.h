@@ -144,8 +144,9 @@ void eval_inputs(const float* X, const uint32_t* t, int n, uint32_t tau, float l
 void normalise_fields(const float* src, float* dst, uint64_t n, float lo, float span, cudaStream_t s);
 
 // Fused head of the paper's network (two hidden layers; d0 <= 8 inputs, hidden widths
-// <= 256 and multiples of 32), HEAD_R batch rows per CTA.
-constexpr int HEAD_R = 8;
+// <= 256 and multiples of 32).  head3_init: once per process (dynamic SMEM attributes).
+int head3_init();
+int head_fwd3_ctas(int B);
 // forward in one launch: the batch inputs gathered from the slot metadata (gather_inputs'
 // arithmetic), Z1/H1, Z2/H2 (+ the bf16 copy of H2); with sd set, the last CTA to finish
 // also computes step_prepare's scalars (world 1, fused Adam) once every bad-input flag is in
@@ -187,7 +188,7 @@ struct HeadBwdArgs {
   double n_field, lr0, lr_min, beta1, beta2;
   uint64_t halving;
 };
-__host__ __device__ inline int head_bwd3_row_ctas(int B) { return (B + HEAD_R - 1) / HEAD_R; }
+__host__ __device__ inline int head_bwd3_row_ctas(int B) { return (B + 31) / 32; }   // row blocks (partials)
 void head_bwd3(const HeadBwdArgs& a, cudaStream_t s);
 size_t head_dw2_part_elems(int B, int d1, int d2);
 

@@ -683,7 +683,7 @@ int step_front(mel_ctx* c) {
       a.sd = c->d_sd; a.n_field = (double)c->N; a.lr0 = c->cfg.lr0; a.lr_min = c->cfg.lr_min;
       a.halving = c->cfg.lr_halving_samples; a.beta1 = c->cfg.beta1; a.beta2 = c->cfg.beta2;
       a.counter = c->d_hcnt;
-      a.target = (c->hf_n + 1) * ((c->B + HEAD_R - 1) / HEAD_R);
+      a.target = (c->hf_n + 1) * (uint32_t)head_fwd3_ctas((int)c->B);
       c->hf_n += 1;
       c->prep_fused = true;
     }
@@ -973,6 +973,7 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
     const char* hf = getenv("MEL_HEAD_FUSED");
     c->head_fused = (!hf || atoi(hf) != 0) && c->L == 3 && c->dims[0] <= 8 && c->dims[1] % 32 == 0 &&
                     c->dims[2] % 32 == 0 && c->dims[1] <= 256 && c->dims[2] <= 256;
+    if (c->head_fused && head3_init() != 0) return fail(c, MEL_ECUDA, "fused head: SMEM attribute rejected");
     if (c->head_fused) {
       const int nrow = head_bwd3_row_ctas((int)c->B);
       DALLOC(c->d_hcnt, 1);

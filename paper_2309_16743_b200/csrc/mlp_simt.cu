@@ -541,104 +541,116 @@ int sgemm_auto(bool ta, bool tb, int M, int N, int K, const float* A, int lda, c
 // Forward: every output is accumulated k ascending from 0, then + bias (the generic sgemm's
 // order without its split-K).  Backward: phase 1 (head_bwd3) writes per-block partial sums,
 // phase 2 (head_fin3) reduces them in a fixed order -- deterministic, no atomics on data.
-constexpr int HKC = 32;          // W2 columns per SMEM chunk (forward)
-constexpr int HWP = HKC + 4;     // its row pitch (float4 reads conflict-free)
-constexpr int HSL = 64;          // batch rows per dW2 slice (backward)
-constexpr int HJT = 16;          // W2 rows per dW2 CTA (backward)
+// Every CTA stages its whole weight / activation block in SMEM with cp.async issued up front
+// (one memory latency per CTA instead of one per chunk: these kernels are latency-bound).
+constexpr int HF_ROWS = 16;      // forward: batch rows per CTA pair (one CTA per 128-unit half)
+constexpr int HF_P = 260;        // forward: W2 row pitch in SMEM (float4 reads conflict-free)
+constexpr int HB_ROWS = 32;      // backward row CTAs: batch rows (x 64 hidden units)
+constexpr int HB_KQ = 64;        // backward row CTAs: layer-1 units per CTA
+constexpr int HSL = 64;          // backward dW2 CTAs: batch rows per slice
+constexpr int HJT = 32;          // backward dW2 CTAs: W2 rows per CTA
+constexpr size_t HF_SMEM = (size_t)(128 * HF_P + HF_ROWS * 256 + HF_ROWS * 8) * 4;
+constexpr size_t HB_SMEM_ROW = (size_t)(256 * HB_KQ + HB_ROWS * 256 + HB_ROWS * 8 + 4 * HB_KQ * 9) * 4 +
+                               (size_t)4 * HB_KQ * 8;
+constexpr size_t HB_SMEM_W2 = (size_t)(HSL * 256 + HSL * HJT) * 4;
+constexpr size_t HB_SMEM = HB_SMEM_ROW > HB_SMEM_W2 ? HB_SMEM_ROW : HB_SMEM_W2;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __global__ void __launch_bounds__(256) head_fwd3_kernel(HeadFwdArgs a) {
   pdl_enter();
-  __shared__ float xs[HEAD_R][8];
-  __shared__ __align__(16) float h1s[HEAD_R][256];
-  __shared__ __align__(16) float ws[256 * HWP];
+  extern __shared__ __align__(16) float hsm[];
+  float* ws = hsm;                                   // [128 units][HF_P]: this half of W2
+  float* h1s = ws + 128 * HF_P;                      // [HF_ROWS][256]
+  float* xs = h1s + HF_ROWS * 256;                   // [HF_ROWS][8]
   const int tid = threadIdx.x;
-  const uint32_t b0 = blockIdx.x * HEAD_R;
+  // CTA pair (2 rb, 2 rb + 1): row block rb, layer-2 units [128 half, 128 half + 128); both
+  // compute layer 1 for the block (6 inputs: cheap), the even one stores it
+  const uint32_t b0 = (blockIdx.x >> 1) * HF_ROWS;
+  const int half = blockIdx.x & 1;
+  const int nu = min(128, a.d2 - 128 * half);        // units of this half (<= 0: none)
+  for (int f = tid; f < 128 * (a.d1 / 4); f += 256) {
+    const int jj = f / (a.d1 / 4), c4 = f % (a.d1 / 4);
+    if (jj < nu) cp_async16(ws + jj * HF_P + 4 * c4, a.W2 + (uint64_t)(128 * half + jj) * a.d1 + 4 * c4);
+  }
   // the batch's normalised inputs (reading Q13), gather_inputs' arithmetic
-  if (tid < HEAD_R) {
+  if (tid < HF_ROWS) {
     const uint32_t b = b0 + tid;
     float out[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (b < a.B) {
       const uint32_t n = a.ra.st->n_last;
       if (b < n) {
-        if (a.ra.bad[a.slots[b]]) atomicOr(&a.ra.st->bad_batch, 1u);     // reset by step_finalize
+        if (half == 0 && a.ra.bad[a.slots[b]]) atomicOr(&a.ra.st->bad_batch, 1u);   // reset by step_finalize
         const SlotMeta m = a.ra.meta[a.slots[b]];
 #pragma unroll
         for (int c = 0; c < 5; ++c) out[c] = normalise_rn(m.X[c], a.ra.lo, a.ra.span);
         out[5] = __fdiv_rn((float)m.t, (float)a.tau);
       }
-      float4* dst = reinterpret_cast<float4*>(a.xn + (uint64_t)b * 8);
-      dst[0] = make_float4(out[0], out[1], out[2], out[3]);
-      dst[1] = make_float4(out[4], out[5], out[6], out[7]);
+      if (half == 0) {
+        float4* dst = reinterpret_cast<float4*>(a.xn + (uint64_t)b * 8);
+        dst[0] = make_float4(out[0], out[1], out[2], out[3]);
+        dst[1] = make_float4(out[4], out[5], out[6], out[7]);
+      }
     }
 #pragma unroll
-    for (int c = 0; c < 8; ++c) xs[tid][c] = out[c];
+    for (int c = 0; c < 8; ++c) xs[tid * 8 + c] = out[c];
   }
-  // W2 [d2][d1] streams through SMEM in HKC-column chunks; the next chunk is fetched into
-  // registers while this one is multiplied
-  constexpr int PER = HKC / 4;   // float4 per thread per chunk (256 rows x HKC columns)
-  float4 pre[PER];
-  auto fetch = [&](int k0) {
-#pragma unroll
-    for (int u = 0; u < PER; ++u) {
-      const int f = tid + 256 * u, jj = f / (HKC / 4), c4 = f % (HKC / 4);
-      pre[u] = jj < a.d2 ? *reinterpret_cast<const float4*>(a.W2 + (uint64_t)jj * a.d1 + k0 + 4 * c4)
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-  };
-  fetch(0);
   __syncthreads();
-  const int nr = (int)min((uint32_t)HEAD_R, a.B > b0 ? a.B - b0 : 0u);
+  const int nr = (int)min((uint32_t)HF_ROWS, a.B > b0 ? a.B - b0 : 0u);
   // layer 1: thread j -> unit j
   if (tid < a.d1) {
     float w[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) w[i] = i < a.d0 ? a.W1[tid * a.d0 + i] : 0.f;
     const float bj = a.b1[tid];
-#pragma unroll
-    for (int r = 0; r < HEAD_R; ++r) {
+#pragma unroll 4
+    for (int r = 0; r < HF_ROWS; ++r) {
       float acc = 0.f;
 #pragma unroll
       for (int i = 0; i < 8; ++i)
-        if (i < a.d0) acc = fmaf(xs[r][i], w[i], acc);
+        if (i < a.d0) acc = fmaf(xs[r * 8 + i], w[i], acc);
       const float z = acc + bj, h = fmaxf(z, 0.f);
-      h1s[r][tid] = h;
-      if (r < nr) {
+      h1s[r * 256 + tid] = h;
+      if (r < nr && half == 0) {
         const uint64_t o = (uint64_t)(b0 + r) * a.d1 + tid;
         a.Z1[o] = z;
         a.H1[o] = h;
       }
     }
   }
-  // layer 2: thread j -> unit j, HEAD_R rows
-  float acc[HEAD_R];
+  cp_async_wait_all();
+  __syncthreads();
+  // layer 2: thread (rq, jl) -> unit 128 half + jl, rows 8 rq .. 8 rq + 7
+  const int jl = tid & 127, rq = tid >> 7;
+  const int j2 = 128 * half + jl;
+  constexpr int R2 = HF_ROWS / 2;
+  float acc[R2];
 #pragma unroll
-  for (int r = 0; r < HEAD_R; ++r) acc[r] = 0.f;
-  for (int k0 = 0; k0 < a.d1; k0 += HKC) {
-    __syncthreads();                                   // previous chunk consumed (h1s complete)
+  for (int r = 0; r < R2; ++r) acc[r] = 0.f;
+  const float* wrow = ws + jl * HF_P;
+  const float* hrow = h1s + R2 * rq * 256;
+#pragma unroll 2
+  for (int k = 0; k < a.d1; k += 4) {
+    const float4 w = *reinterpret_cast<const float4*>(wrow + k);
 #pragma unroll
-    for (int u = 0; u < PER; ++u) {
-      const int f = tid + 256 * u, jj = f / (HKC / 4), c4 = f % (HKC / 4);
-      *reinterpret_cast<float4*>(&ws[jj * HWP + 4 * c4]) = pre[u];
-    }
-    __syncthreads();
-    if (k0 + HKC < a.d1) fetch(k0 + HKC);
-#pragma unroll
-    for (int kk = 0; kk < HKC; kk += 4) {
-      const float4 w = *reinterpret_cast<const float4*>(&ws[tid * HWP + kk]);
-#pragma unroll
-      for (int r = 0; r < HEAD_R; ++r) {
-        const float4 h = *reinterpret_cast<const float4*>(&h1s[r][k0 + kk]);
-        acc[r] = fmaf(h.x, w.x, acc[r]);
-        acc[r] = fmaf(h.y, w.y, acc[r]);
-        acc[r] = fmaf(h.z, w.z, acc[r]);
-        acc[r] = fmaf(h.w, w.w, acc[r]);
-      }
+    for (int r = 0; r < R2; ++r) {
+      const float4 h = *reinterpret_cast<const float4*>(hrow + r * 256 + k);
+      acc[r] = fmaf(h.x, w.x, acc[r]);
+      acc[r] = fmaf(h.y, w.y, acc[r]);
+      acc[r] = fmaf(h.z, w.z, acc[r]);
+      acc[r] = fmaf(h.w, w.w, acc[r]);
     }
   }
-  if (tid < a.d2) {
-    const float bj = a.b2[tid];
-    for (int r = 0; r < nr; ++r) {
-      const uint64_t o = (uint64_t)(b0 + r) * a.d2 + tid;
+  if (jl < nu) {
+    const float bj = a.b2[j2];
+#pragma unroll
+    for (int r = 0; r < R2; ++r) {
+      if (R2 * rq + r >= nr) break;
+      const uint64_t o = (uint64_t)(b0 + R2 * rq + r) * a.d2 + j2;
       const float z = acc[r] + bj, h = fmaxf(z, 0.f);
       a.Z2[o] = z;
       a.H2[o] = h;
@@ -658,112 +670,126 @@ __global__ void __launch_bounds__(256) head_fwd3_kernel(HeadFwdArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(256) head_bwd3_kernel(HeadBwdArgs a) {
+__global__ void __launch_bounds__(256, 2) head_bwd3_kernel(HeadBwdArgs a) {
   pdl_enter();
-  __shared__ __align__(16) float sm[HEAD_R * 256 + HEAD_R * 8];
+  extern __shared__ __align__(16) float hsm[];
   const int tid = threadIdx.x;
-  const int n_row = head_bwd3_row_ctas(a.B);
-  if ((int)blockIdx.x < n_row) {
-    // ===== row CTA: dZ1 = (dZ2 W2) . ReLU'(Z1) for HEAD_R rows; partial dW1 / db1 =====
-    float* dz = sm;                                    // [HEAD_R][256]
-    float* xs = sm + HEAD_R * 256;                     // [HEAD_R][8]
-    const int b0 = blockIdx.x * HEAD_R;
-    const int nr = min(HEAD_R, a.B - b0);
-    for (int i = tid; i < HEAD_R * 256; i += 256) {
-      const int r = i / 256, j = i % 256;
-      dz[i] = (r < nr && j < a.d2) ? a.dz2[(uint64_t)(b0 + r) * a.d2 + j] : 0.f;
+  const int n_kq = (a.d1 + HB_KQ - 1) / HB_KQ;
+  const int n_rowc = head_bwd3_row_ctas(a.B) * n_kq;
+  if ((int)blockIdx.x < n_rowc) {
+    // ===== row CTA: dZ1 = (dZ2 W2) . ReLU'(Z1) for HB_ROWS rows x HB_KQ units; partial
+    // dW1 / db1 of the row block =====
+    float* ws = hsm;                                 // [256 j][HB_KQ]: W2[:, this quarter]
+    float* dz = ws + 256 * HB_KQ;                    // [HB_ROWS][256]
+    float* xs = dz + HB_ROWS * 256;                  // [HB_ROWS][8]
+    float* pw_s = xs + HB_ROWS * 8;                  // [4 row groups][HB_KQ][9]
+    double* pdb_s = reinterpret_cast<double*>(pw_s + 4 * HB_KQ * 9);   // [4][HB_KQ]
+    const int rb = blockIdx.x / n_kq, kq = blockIdx.x % n_kq;
+    const int b0 = rb * HB_ROWS, k0 = kq * HB_KQ;
+    const int nr = min(HB_ROWS, a.B - b0), nk = min(HB_KQ, a.d1 - k0);
+    for (int f = tid; f < a.d2 * (HB_KQ / 4); f += 256) {
+      const int j = f / (HB_KQ / 4), c4 = f % (HB_KQ / 4);
+      if (4 * c4 < nk) cp_async16(ws + j * HB_KQ + 4 * c4, a.W2 + (uint64_t)j * a.d1 + k0 + 4 * c4);
     }
-    if (tid < HEAD_R * 8) {
+    for (int f = tid; f < HB_ROWS * (a.d2 / 4); f += 256) {
+      const int r = f / (a.d2 / 4), c4 = f % (a.d2 / 4);
+      if (r < nr) cp_async16(dz + r * 256 + 4 * c4, a.dz2 + (uint64_t)(b0 + r) * a.d2 + 4 * c4);
+      else *reinterpret_cast<float4*>(dz + r * 256 + 4 * c4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    {
       const int r = tid / 8, i = tid % 8;
       xs[tid] = r < nr ? a.xn[(uint64_t)(b0 + r) * 8 + i] : 0.f;
     }
-    const int k = tid < a.d1 ? tid : 0;
-    // W2 column k in 16-row chunks through registers (coalesced across k), one chunk ahead
-    float wn[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) wn[u] = u < a.d2 ? a.W2[(uint64_t)u * a.d1 + k] : 0.f;
+    cp_async_wait_all();
     __syncthreads();
-    float acc[HEAD_R];
+    const int kl = tid % HB_KQ, rg = tid / HB_KQ;    // unit k0 + kl, rows 8 rg .. 8 rg + 7
+    const int k = k0 + kl;
+    float acc[8];
 #pragma unroll
-    for (int r = 0; r < HEAD_R; ++r) acc[r] = 0.f;
-    for (int j0 = 0; j0 < a.d2; j0 += 16) {
-      float w[16];
+    for (int r = 0; r < 8; ++r) acc[r] = 0.f;
+    const float* drow = dz + 8 * rg * 256;
+#pragma unroll 2
+    for (int j = 0; j < a.d2; j += 4) {
+      const float w0 = ws[j * HB_KQ + kl], w1 = ws[(j + 1) * HB_KQ + kl];
+      const float w2 = ws[(j + 2) * HB_KQ + kl], w3 = ws[(j + 3) * HB_KQ + kl];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) w[u] = wn[u];
-      if (j0 + 16 < a.d2) {
-#pragma unroll
-        for (int u = 0; u < 16; ++u) wn[u] = a.W2[(uint64_t)(j0 + 16 + u) * a.d1 + k];
-      }
-#pragma unroll
-      for (int u = 0; u < 16; u += 4) {
-#pragma unroll
-        for (int r = 0; r < HEAD_R; ++r) {
-          const float4 d = *reinterpret_cast<const float4*>(&dz[r * 256 + j0 + u]);
-          acc[r] = fmaf(d.x, w[u], acc[r]);
-          acc[r] = fmaf(d.y, w[u + 1], acc[r]);
-          acc[r] = fmaf(d.z, w[u + 2], acc[r]);
-          acc[r] = fmaf(d.w, w[u + 3], acc[r]);
-        }
+      for (int r = 0; r < 8; ++r) {
+        const float4 d = *reinterpret_cast<const float4*>(drow + r * 256 + j);
+        acc[r] = fmaf(d.x, w0, acc[r]);
+        acc[r] = fmaf(d.y, w1, acc[r]);
+        acc[r] = fmaf(d.z, w2, acc[r]);
+        acc[r] = fmaf(d.w, w3, acc[r]);
       }
     }
-    if (tid < a.d1) {
-      float pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      double pdb = 0.0;
+    float pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    double pdb = 0.0;
+    if (kl < nk) {
 #pragma unroll
-      for (int r = 0; r < HEAD_R; ++r) {
-        if (r >= nr) break;
-        const float d = a.z1[(uint64_t)(b0 + r) * a.d1 + k] > 0.f ? acc[r] : 0.f;   // ReLU'(0) = 0 (R20)
+      for (int r = 0; r < 8; ++r) {
+        const int rr = 8 * rg + r;
+        if (rr >= nr) break;
+        const float d = a.z1[(uint64_t)(b0 + rr) * a.d1 + k] > 0.f ? acc[r] : 0.f;   // ReLU'(0) = 0 (R20)
         pdb += (double)d;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) pw[i] = fmaf(d, xs[r * 8 + i], pw[i]);
+        for (int i = 0; i < 8; ++i) pw[i] = fmaf(d, xs[rr * 8 + i], pw[i]);
       }
-      float4* dst = reinterpret_cast<float4*>(a.p_dw1 + ((uint64_t)blockIdx.x * a.d1 + k) * 8);
-      dst[0] = make_float4(pw[0], pw[1], pw[2], pw[3]);
-      dst[1] = make_float4(pw[4], pw[5], pw[6], pw[7]);
-      a.p_db1[(uint64_t)blockIdx.x * a.d1 + k] = pdb;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) pw_s[(rg * HB_KQ + kl) * 9 + i] = pw[i];
+    pdb_s[rg * HB_KQ + kl] = pdb;
+    __syncthreads();
+    if (tid < HB_KQ && tid < nk) {
+      // the block's four row groups in order
+      float t[8];
+      double tb = 0.0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) t[i] = 0.f;
+      for (int g = 0; g < 4; ++g) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) t[i] += pw_s[(g * HB_KQ + tid) * 9 + i];
+        tb += pdb_s[g * HB_KQ + tid];
+      }
+      float4* dst = reinterpret_cast<float4*>(a.p_dw1 + ((uint64_t)rb * a.d1 + k0 + tid) * 8);
+      dst[0] = make_float4(t[0], t[1], t[2], t[3]);
+      dst[1] = make_float4(t[4], t[5], t[6], t[7]);
+      a.p_db1[(uint64_t)rb * a.d1 + k0 + tid] = tb;
     }
     return;
   }
   // ===== dW2 CTA: slice sl (HSL batch rows) x W2 rows [HJT jt, HJT jt + HJT): partial
   // dW2[j][k] = sum_b dZ2[b][j] H1[b][k] (thread k), partial db2 (fp64) =====
-  const int w = blockIdx.x - n_row;
+  const int w = blockIdx.x - n_rowc;
   const int njt = a.d2 / HJT;
   const int sl = w / njt, jt = w % njt;
-  const int bs = sl * HSL, be = min(a.B, bs + HSL);
-  float* dzs = sm;                                      // [HSL][HJT]
-  for (int i = tid; i < HSL * HJT; i += 256) {
-    const int r = i / HJT, j = i % HJT, b = bs + r;
-    dzs[i] = b < be ? a.dz2[(uint64_t)b * a.d2 + jt * HJT + j] : 0.f;
+  const int bs = sl * HSL, nb = min(HSL, a.B - bs);
+  float* hs = hsm;                                     // [HSL][256]
+  float* dzs = hs + HSL * 256;                         // [HSL][HJT]
+  for (int f = tid; f < HSL * (a.d1 / 4); f += 256) {
+    const int r = f / (a.d1 / 4), c4 = f % (a.d1 / 4);
+    if (r < nb) cp_async16(hs + r * 256 + 4 * c4, a.h1 + (uint64_t)(bs + r) * a.d1 + 4 * c4);
+    else *reinterpret_cast<float4*>(hs + r * 256 + 4 * c4) = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  const int k = tid < a.d1 ? tid : 0;
-  float hn[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) hn[u] = bs + u < be ? a.h1[(uint64_t)(bs + u) * a.d1 + k] : 0.f;
+  for (int f = tid; f < HSL * (HJT / 4); f += 256) {
+    const int r = f / (HJT / 4), c4 = f % (HJT / 4);
+    if (r < nb) cp_async16(dzs + r * HJT + 4 * c4, a.dz2 + (uint64_t)(bs + r) * a.d2 + jt * HJT + 4 * c4);
+    else *reinterpret_cast<float4*>(dzs + r * HJT + 4 * c4) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  cp_async_wait_all();
   __syncthreads();
+  const int k = tid < a.d1 ? tid : 0;
   float acc[HJT];
 #pragma unroll
   for (int j = 0; j < HJT; ++j) acc[j] = 0.f;
-  for (int r0 = 0; r0 < HSL; r0 += 8) {
-    float h[8];
+#pragma unroll 2
+  for (int r = 0; r < HSL; ++r) {
+    const float h = hs[r * 256 + k];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) h[u] = hn[u];
-    if (r0 + 8 < HSL) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int b = bs + r0 + 8 + u;
-        hn[u] = b < be ? a.h1[(uint64_t)b * a.d1 + k] : 0.f;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-#pragma unroll
-      for (int j = 0; j < HJT; j += 4) {
-        const float4 d = *reinterpret_cast<const float4*>(&dzs[(r0 + u) * HJT + j]);
-        acc[j] = fmaf(d.x, h[u], acc[j]);
-        acc[j + 1] = fmaf(d.y, h[u], acc[j + 1]);
-        acc[j + 2] = fmaf(d.z, h[u], acc[j + 2]);
-        acc[j + 3] = fmaf(d.w, h[u], acc[j + 3]);
-      }
+    for (int j = 0; j < HJT; j += 4) {
+      const float4 d = *reinterpret_cast<const float4*>(&dzs[r * HJT + j]);
+      acc[j] = fmaf(d.x, h, acc[j]);
+      acc[j + 1] = fmaf(d.y, h, acc[j + 1]);
+      acc[j + 2] = fmaf(d.z, h, acc[j + 2]);
+      acc[j + 3] = fmaf(d.w, h, acc[j + 3]);
     }
   }
   if (tid < a.d1) {
@@ -784,27 +810,56 @@ __global__ void __launch_bounds__(256) head_fin3_kernel(HeadBwdArgs a) {
   pdl_enter();
   __shared__ double sred[256];
   const int n_row = head_bwd3_row_ctas(a.B), n_sl = (a.B + HSL - 1) / HSL;
-  const int n_w2 = a.d2 * a.d1, n_w1 = a.d1 * a.d0;
-  const int o = blockIdx.x * 256 + threadIdx.x;
-  if (o < n_w2) {
-    float t = 0.f;
-    for (int c = 0; c < n_sl; ++c) t += a.p_dw2[(uint64_t)c * n_w2 + o];
-    a.gW2[o] = t;
-  } else if (o < n_w2 + n_w1) {
-    const int q = o - n_w2, k = q / a.d0, i = q % a.d0;
-    float t = 0.f;
-    for (int c = 0; c < n_row; ++c) t += a.p_dw1[((uint64_t)c * a.d1 + k) * 8 + i];
-    a.gW1[q] = t;
-  } else if (o < n_w2 + n_w1 + a.d1) {
-    const int k = o - n_w2 - n_w1;
-    double t = 0.0;
-    for (int c = 0; c < n_row; ++c) t += a.p_db1[(uint64_t)c * a.d1 + k];
-    a.gb1[k] = (float)t;
-  } else if (o < n_w2 + n_w1 + a.d1 + a.d2) {
-    const int j = o - n_w2 - n_w1 - a.d1;
-    double t = 0.0;
-    for (int c = 0; c < n_sl; ++c) t += a.p_db2[(uint64_t)c * a.d2 + j];
-    a.gb2[j] = (float)t;
+  const int n_w2 = a.d2 * a.d1;
+  const int nb_w2 = (n_w2 + 255) / 256;
+  if ((int)blockIdx.x < nb_w2) {
+    // dW2: one output per thread, the slice partials in slice order (loads all in flight)
+    const int o = blockIdx.x * 256 + threadIdx.x;
+    if (o < n_w2) {
+      float t = 0.f;
+      for (int c0 = 0; c0 < n_sl; c0 += 16) {
+        float v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = c0 + u < n_sl ? __ldcg(a.p_dw2 + (uint64_t)(c0 + u) * n_w2 + o) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) t += v[u];
+      }
+      a.gW2[o] = t;
+    }
+  } else {
+    // dW1 / db1 (row-CTA partials) and db2 (slice partials): one warp per unit k; lane l
+    // takes partials l, l + 32, ... in order, then a fixed xor-butterfly across the warp
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int k = ((int)blockIdx.x - nb_w2) * 8 + warp;
+    if (k < a.d1 || k < a.d2) {
+      float pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      double pdb1 = 0.0, pdb2 = 0.0;
+      if (k < a.d1) {
+        for (int c = lane; c < n_row; c += 32) {
+          const float4* src = reinterpret_cast<const float4*>(a.p_dw1 + ((uint64_t)c * a.d1 + k) * 8);
+          const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
+          pw[0] += x0.x; pw[1] += x0.y; pw[2] += x0.z; pw[3] += x0.w;
+          pw[4] += x1.x; pw[5] += x1.y; pw[6] += x1.z; pw[7] += x1.w;
+          pdb1 += __ldcg(a.p_db1 + (uint64_t)c * a.d1 + k);
+        }
+      }
+      if (k < a.d2)
+        for (int c = lane; c < n_sl; c += 32) pdb2 += __ldcg(a.p_db2 + (uint64_t)c * a.d2 + k);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) pw[i] += __shfl_xor_sync(0xffffffffu, pw[i], o);
+        pdb1 += __shfl_xor_sync(0xffffffffu, pdb1, o);
+        pdb2 += __shfl_xor_sync(0xffffffffu, pdb2, o);
+      }
+      if (lane == 0) {
+        if (k < a.d1) {
+          for (int i = 0; i < a.d0; ++i) a.gW1[k * a.d0 + i] = pw[i];
+          a.gb1[k] = (float)pdb1;
+        }
+        if (k < a.d2) a.gb2[k] = (float)pdb2;
+      }
+    }
   }
   if (a.sd && blockIdx.x == 0) {
     reduce_local_block(a.sd, a.sse_parts, a.n_sse_parts, a.st, sred);
@@ -814,15 +869,25 @@ __global__ void __launch_bounds__(256) head_fin3_kernel(HeadBwdArgs a) {
   }
 }
 
+int head3_init() {
+  if (cudaFuncSetAttribute(head_fwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HF_SMEM) != cudaSuccess)
+    return -1;
+  if (cudaFuncSetAttribute(head_bwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HB_SMEM) != cudaSuccess)
+    return -1;
+  return 0;
+}
+
+int head_fwd3_ctas(int B) { return 2 * ((B + HF_ROWS - 1) / HF_ROWS); }
+
 void head_fwd3(const HeadFwdArgs& a, cudaStream_t s) {
-  launch_pdl(head_fwd3_kernel, dim3((a.B + HEAD_R - 1) / HEAD_R), dim3(256), 0, s, a);
+  launch_pdl(head_fwd3_kernel, dim3(head_fwd3_ctas((int)a.B)), dim3(256), HF_SMEM, s, a);
 }
 
 void head_bwd3(const HeadBwdArgs& a, cudaStream_t s) {
-  const int n = head_bwd3_row_ctas(a.B) + ((a.B + HSL - 1) / HSL) * (a.d2 / HJT);
-  launch_pdl(head_bwd3_kernel, dim3(n), dim3(256), 0, s, a);
-  const int n_out = a.d2 * a.d1 + a.d1 * a.d0 + a.d1 + a.d2;
-  launch_pdl(head_fin3_kernel, dim3((n_out + 255) / 256), dim3(256), 0, s, a);
+  const int n = head_bwd3_row_ctas(a.B) * ((a.d1 + HB_KQ - 1) / HB_KQ) + ((a.B + HSL - 1) / HSL) * (a.d2 / HJT);
+  launch_pdl(head_bwd3_kernel, dim3(n), dim3(256), HB_SMEM, s, a);
+  const int nb = (a.d2 * a.d1 + 255) / 256 + ((a.d1 > a.d2 ? a.d1 : a.d2) + 7) / 8;
+  launch_pdl(head_fin3_kernel, dim3(nb), dim3(256), 0, s, a);
 }
 
 size_t head_dw2_part_elems(int B, int d1, int d2) { return (size_t)((B + HSL - 1) / HSL) * d1 * d2; }
