@@ -147,10 +147,44 @@ def run_reference(args, rank, world):
 # our arm
 # ------------------------------------------------------------------------------------
 class Clocks:
+    """SM clocks and clock-event (throttle) reasons sampled during the timed region: NVML
+    (what nvidia-smi reads) polled every 2 ms from a thread, only samples taken between
+    __enter__ and __exit__ kept; nvidia-smi -lms 20 as the fallback without pynvml."""
+
+    REASONS = [("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap")]
+
     def __init__(self, idx):
         self.idx, self.p, self.path = idx, None, "/tmp/mel_clocks_%d.csv" % os.getpid()
+        self.nv, self.rows, self.err = None, [], None
 
     def __enter__(self):
+        try:
+            import threading
+
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.idx)
+            self.nv, self.stop = nv, threading.Event()
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((sm, mx, rs))
+                    except Exception as e:          # keep sampling; report the last error
+                        self.err = str(e)
+                    self.stop.wait(0.002)
+
+            self.th = threading.Thread(target=poll, daemon=True)
+            self.th.start()
+            return self
+        except Exception:
+            self.nv = None
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -164,6 +198,10 @@ class Clocks:
         return self
 
     def __exit__(self, *a):
+        if self.nv is not None:
+            self.stop.set()
+            self.th.join()
+            return
         if self.p:
             time.sleep(0.05)
             self.p.terminate()
@@ -171,6 +209,19 @@ class Clocks:
             self.f.close()
 
     def summary(self):
+        if self.nv is not None:
+            if not self.rows:
+                return {"error": "no NVML sample inside the timed region" + (": " + self.err if self.err else "")}
+            sm = [float(r[0]) for r in self.rows]
+            mx = float(max(r[1] for r in self.rows))
+            reasons = set()
+            for _, _, rs in self.rows:
+                for name, attr in self.REASONS:
+                    if rs & getattr(self.nv, attr, 0):
+                        reasons.add(name)
+            loaded = [s for s in sm if s > 0.5 * mx] or sm
+            return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                    "samples": len(sm), "source": "nvml, 2 ms"}
         try:
             rows = [[x.strip() for x in l.split(",")] for l in open(self.path).read().strip().splitlines()]
             rows = [r for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
@@ -185,7 +236,7 @@ class Clocks:
                         reasons.add(name)
             loaded = [s for s in sm if s > 0.5 * mx] or sm
             return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                    "samples": len(sm)}
+                    "samples": len(sm), "source": "nvidia-smi -lms 20"}
         except Exception as e:
             return {"error": str(e)}
 
