@@ -57,6 +57,27 @@ __device__ __forceinline__ float normalise_rn(float u, float lo, float span) {
   return __fdiv_rn(__fsub_rn(u, lo), span);
 }
 
+// One Adam element in the PyTorch form (the step scalars from StepDev):
+//   m' = b1 m + (1 - b1) g,  v' = b2 v + (1 - b2) g^2,  p' = p - step m' / (sqrt(v') isc2 + eps)
+// with step = lr / (1 - b1^k) and isc2 = 1 / sqrt(1 - b2^k).  The square root and the
+// division use the SFU (sqrt.approx, rcp.approx: a few ulp, reading R26); the separate Adam
+// kernel and the one fused into K1 call this same function, so they agree bit for bit.  An
+// element whose new second moment would not be finite (a non-finite gradient or one whose
+// square overflows) keeps p, m, v (include/mel.h surrogate_step).
+__device__ __forceinline__ void adam_elem(float& p, float& m, float& v, float g, float scale, float step, float isc2,
+                                          float b1, float b2, float eps) {
+  const float gr = g * scale;
+  const float nv = fmaf(b2, v, (1.f - b2) * gr * gr);
+  if (!(nv < __int_as_float(0x7f800000))) return;
+  const float nm = fmaf(b1, m, (1.f - b1) * gr);
+  float s, r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(nv));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fmaf(s, isc2, eps)));
+  p = fmaf(-step, nm * r, p);
+  m = nm;
+  v = nv;
+}
+
 __device__ __forceinline__ float bf16_bits_to_f32(uint16_t h) {
   return __uint_as_float(((uint32_t)h) << 16);
 }

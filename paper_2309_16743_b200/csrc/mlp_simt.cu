@@ -352,20 +352,9 @@ __global__ void step_prepare_kernel(StepDev* sd, const ResDev* st, double n_fiel
 // Two float4 per array in flight per thread (memory-level parallelism).
 __device__ __forceinline__ void adam4(float4& pp, float4& mm, float4& vv, const float4& gg, float scale, float step,
                                       float inv_sqrt_c2, float b1, float b2, float eps) {
-  // PyTorch form: denom = sqrt(v) / sqrt(1 - b2^k) + eps;  p -= (lr / (1 - b1^k)) * m / denom
   float* P = &pp.x; float* Mv = &mm.x; float* V = &vv.x; const float* G = &gg.x;
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const float gr = G[c] * scale;
-    const float nv = fmaf(b2, V[c], (1.f - b2) * gr * gr);
-    // an element whose second moment would not be finite (a non-finite gradient, or one whose
-    // square overflows) keeps p, m, v as they are (include/mel.h surrogate_step)
-    if (!isfinite(nv)) continue;
-    Mv[c] = fmaf(b1, Mv[c], (1.f - b1) * gr);
-    V[c] = nv;
-    const float denom = fmaf(__fsqrt_rn(V[c]), inv_sqrt_c2, eps);
-    P[c] = fmaf(-step, __fdiv_rn(Mv[c], denom), P[c]);
-  }
+  for (int c = 0; c < 4; ++c) adam_elem(P[c], Mv[c], V[c], G[c], scale, step, inv_sqrt_c2, b1, b2, eps);
 }
 
 __device__ __forceinline__ void store_shadow(__nv_bfloat16* shadow, uint64_t e, uint64_t b0, uint64_t b1,
