@@ -90,6 +90,9 @@ struct ResArgs {
 // reservoir.cu
 void launch_commit(const ResArgs& a, uint64_t tail, uint32_t closed, uint32_t max_entries, cudaStream_t s);
 void launch_sample(const ResArgs& a, int32_t* slots, uint32_t B, cudaStream_t s);
+// Reservoir policy: commit control + sample in one launch, then the commit's data plane
+void launch_commit_sample(const ResArgs& a, uint64_t tail, uint32_t closed, uint32_t max_entries, int32_t* slots,
+                          uint32_t B, cudaStream_t s);
 void launch_gather(const ResArgs& a, const int32_t* slots, uint32_t B, uint32_t tau, float* xn, cudaStream_t s);
 void launch_init_res(const ResArgs& a, cudaStream_t s);
 

@@ -1580,14 +1580,30 @@ int reservoir_close(mel_ctx* c) {
 
 int reservoir_sample_batch(mel_ctx* c, int32_t* slots_host, uint32_t* n_host) {
   GUARD(c);
-  int r = commit(c);
-  if (r) return r;
-  {
-    Timer t(c, MEL_K_SAMPLE, 1);
-    launch_sample(c->ra, c->d_slots, c->Bs, c->stream);
+  int r;
+  if (c->cfg.policy == MEL_RESERVOIR) {
+    // commit control and the draws in one launch, then the commit's data plane
+    const uint64_t max_e = c->tail - c->known_consumed;
+    if (c->copy_pending) {
+      CK(cudaStreamWaitEvent(c->stream, c->ev_copy, 0));
+      c->copy_pending = false;
+    }
+    {
+      Timer t(c, MEL_K_COMMIT, max_e ? 2 : 1);
+      launch_commit_sample(c->ra, c->tail, c->closed ? 1u : 0u, (uint32_t)max_e, c->d_slots, c->Bs, c->stream);
+    }
+    r = check_launch(c, "commit + sample");
+    if (r) return r;
+  } else {
+    r = commit(c);
+    if (r) return r;
+    {
+      Timer t(c, MEL_K_SAMPLE, 1);
+      launch_sample(c->ra, c->d_slots, c->Bs, c->stream);
+    }
+    r = check_launch(c, "sample");
+    if (r) return r;
   }
-  r = check_launch(c, "sample");
-  if (r) return r;
   // During reception the fill phase never blocks (u <= p < C), so p = min(C, puts)
   // at every commit point and the watermark gate is host-decidable.
   bool need_sync = slots_host || n_host || c->closed;

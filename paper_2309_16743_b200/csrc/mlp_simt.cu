@@ -122,6 +122,39 @@ __global__ void splitk_reduce_kernel(int M, int N, int splits, const float* __re
   }
 }
 
+// The same reduction, 4 consecutive columns per thread (N, ldc, ldm multiples of 4, 16-byte
+// aligned pointers): float4 loads of 8 splits are issued before the 8 adds, which still run
+// in split order (bit-identical to splitk_reduce_kernel; that one waited on every load)
+__global__ void splitk_reduce4_kernel(int M, int N, int splits, const float4* __restrict__ part, float* __restrict__ C,
+                                      int ldc, const float* __restrict__ mask, int ldm) {
+  pdl_enter();
+  const size_t total4 = (size_t)M * N / 4, stride = total4;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total4; i += (size_t)gridDim.x * blockDim.x) {
+    const int m = (int)(4 * i / N), n = (int)(4 * i % N);
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    int z = 0;
+    for (; z + 8 <= splits; z += 8) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(part + (size_t)(z + u) * stride + i);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { s.x += v[u].x; s.y += v[u].y; s.z += v[u].z; s.w += v[u].w; }
+    }
+    for (; z < splits; ++z) {
+      const float4 v = __ldg(part + (size_t)z * stride + i);
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    if (mask) {                                                          // ReLU'(0) = 0
+      const float4 mk = *reinterpret_cast<const float4*>(mask + (size_t)m * ldm + n);
+      if (!(mk.x > 0.f)) s.x = 0.f;
+      if (!(mk.y > 0.f)) s.y = 0.f;
+      if (!(mk.z > 0.f)) s.z = 0.f;
+      if (!(mk.w > 0.f)) s.w = 0.f;
+    }
+    *reinterpret_cast<float4*>(C + (size_t)m * ldc + n) = s;
+  }
+}
+
 // Output layer, fp32 parity mode: Y = H W^T + b, raw gradient dS/dY = 2 (Y - T)
 // for valid rows/cols (0 elsewhere), SSE partial per block.
 __global__ void __launch_bounds__(256)
@@ -487,7 +520,13 @@ void sgemm(bool ta, bool tb, int M, int N, int K, const float* A, int lda, const
 
 void splitk_reduce(int M, int N, int splits, const float* part, float* C, int ldc, const float* relu_mask, int ldm,
                    cudaStream_t s) {
-  launch_pdl(splitk_reduce_kernel, dim3(grid_for((uint64_t)M * N)), dim3(256), 0, s, M, N, splits, part, C, ldc, relu_mask, ldm);
+  const bool v4 = N % 4 == 0 && ldc % 4 == 0 && (!relu_mask || ldm % 4 == 0) && ((uintptr_t)part & 15) == 0 &&
+                  ((uintptr_t)C & 15) == 0 && ((uintptr_t)relu_mask & 15) == 0;
+  if (v4)
+    launch_pdl(splitk_reduce4_kernel, dim3(grid_for((uint64_t)M * N / 4)), dim3(256), 0, s, M, N, splits,
+               reinterpret_cast<const float4*>(part), C, ldc, relu_mask, ldm);
+  else
+    launch_pdl(splitk_reduce_kernel, dim3(grid_for((uint64_t)M * N)), dim3(256), 0, s, M, N, splits, part, C, ldc, relu_mask, ldm);
 }
 
 int out_fwd_f32(const OutArgs& a, cudaStream_t s) {

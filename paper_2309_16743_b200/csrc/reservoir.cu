@@ -11,6 +11,8 @@
 //   sample_kernel: B Philox SAMPLE(d+b) draws with replacement,
 //                  seen counters by atomicAdd (order-free), u -= #(0->1); after
 //                  the reception is over, sequential DRAIN draws with removal.
+//   commit_sample_kernel: reservoir_sample_batch's commit control and draws in one
+//                  launch (Reservoir policy), before the commit's copy grid.
 //   gather_inputs: normalised network inputs (X, t) of the batch (reading Q13).
 // The comparison buffers of P:221-223 (reading R21) reuse the same put / staging /
 // commit machinery: commit appends while p < C (FIFO at ring slot head + p, FIRO at
@@ -81,13 +83,9 @@ __device__ void commit_queue(const ResArgs& a, uint64_t tail, uint32_t closed) {
   }
 }
 
-__global__ void __launch_bounds__(CTRL_THREADS, 1)
-commit_ctrl(ResArgs a, uint64_t tail, uint32_t closed) {
-  pdl_enter();
-  if (a.policy != 0) {
-    commit_queue(a, tail, closed);
-    return;
-  }
+// Reservoir commit control (one CTA of CTRL_THREADS): the body of commit_ctrl and of the
+// first half of commit_sample_kernel
+__device__ __forceinline__ void commit_reservoir(const ResArgs& a, uint64_t tail, uint32_t closed) {
   // Seen bitmap + exclusive prefix of its word popcounts in SMEM.  One warp plans the
   // puts in order (fill slots p, p+1, ...; full phase: evict the r-th seen slot, found by
   // a binary search over the prefix and a find-n-th-set-bit, then the prefix updated
@@ -100,10 +98,23 @@ commit_ctrl(ResArgs a, uint64_t tail, uint32_t closed) {
   __shared__ uint32_t s_warp[32];
   __shared__ uint32_t s_res[3];                  // p, u, n_plan after planning (thread 0 -> block)
   __shared__ uint32_t s_nev;
-  for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) s_bits[i] = a.bitmap[i];
+  // the first CC_PF pending entries' metadata and source pointers live in mapped host
+  // memory: their loads are issued first, so the PCIe round trip overlaps the bitmap scan
+  // and the planning instead of following them
+  constexpr uint32_t CC_PF = 256;
+  __shared__ StMeta s_meta[CC_PF];
+  __shared__ const float* s_src[CC_PF];
   ResDev* st = a.st;
+  const uint64_t c0 = st->consumed;
+  const uint64_t n_pf = tail - c0 < CC_PF ? tail - c0 : CC_PF;
+  if (threadIdx.x < n_pf) {
+    const uint32_t e = (uint32_t)((c0 + threadIdx.x) % a.S);
+    s_meta[threadIdx.x] = a.st_meta[e];
+    s_src[threadIdx.x] = a.st_src[e];
+  }
+  for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) s_bits[i] = a.bitmap[i];
   uint32_t p = st->p, u = st->u;
-  const uint64_t q0 = st->q, c0 = st->consumed;
+  const uint64_t q0 = st->q;
   __syncthreads();
   {
     const uint32_t wpt = (W + blockDim.x - 1) / blockDim.x;   // words per thread
@@ -163,15 +174,13 @@ commit_ctrl(ResArgs a, uint64_t tail, uint32_t closed) {
       const uint32_t sc = a.seen[j];
       atomicAdd(reinterpret_cast<unsigned long long*>(&st->hist[sc < HIST_BINS ? sc : HIST_BINS - 1]), 1ull);
     }
-    a.meta[j] = a.st_meta[ej.x];
-    {
-      const float* X = a.st_meta[ej.x].X;
-      a.bad[j] = (isfinite(X[0]) && isfinite(X[1]) && isfinite(X[2]) && isfinite(X[3]) && isfinite(X[4])) ? 0u : 1u;
-    }
+    const StMeta m = i < CC_PF ? s_meta[i] : a.st_meta[ej.x];     // plan entry i is pending entry c0 + i
+    a.meta[j] = m;
+    a.bad[j] = (isfinite(m.X[0]) && isfinite(m.X[1]) && isfinite(m.X[2]) && isfinite(m.X[3]) && isfinite(m.X[4])) ? 0u : 1u;
     a.seen[j] = 0;
     a.put_seq[j] = q0 + i;
     a.plan[i] = make_uint2(ej.x, j);
-    a.plan_src[i] = a.st_src[ej.x];
+    a.plan_src[i] = i < CC_PF ? s_src[i] : a.st_src[ej.x];
   }
   if (threadIdx.x == 0) st->evictions += s_nev;
   __syncthreads();
@@ -183,6 +192,13 @@ commit_ctrl(ResArgs a, uint64_t tail, uint32_t closed) {
     m->consumed = consumed; m->q = q; m->p = p; m->u = u; m->over = st->over;
     m->evictions = st->evictions; m->d = st->d;
   }
+}
+
+__global__ void __launch_bounds__(CTRL_THREADS, 1)
+commit_ctrl(ResArgs a, uint64_t tail, uint32_t closed) {
+  pdl_enter();
+  if (a.policy != 0) commit_queue(a, tail, closed);
+  else commit_reservoir(a, tail, closed);
 }
 
 // data plane: blockIdx.y = plan index, 4 floats per thread per iteration
@@ -293,9 +309,7 @@ firo_sample_kernel(ResArgs a, int32_t* slots, uint32_t B) {
   if (threadIdx.x == 0) finish_queue_batch(a, p, n, d + n);
 }
 
-__global__ void __launch_bounds__(SAMPLE_THREADS, 1)
-sample_kernel(ResArgs a, int32_t* slots, uint32_t B) {
-  pdl_enter();
+__device__ __forceinline__ void sample_reservoir(const ResArgs& a, int32_t* slots, uint32_t B) {
   __shared__ uint32_t s_cnt;
   ResDev* st = a.st;
   if (threadIdx.x == 0) s_cnt = 0;
@@ -347,6 +361,25 @@ sample_kernel(ResArgs a, int32_t* slots, uint32_t B) {
   }
 }
 
+__global__ void __launch_bounds__(SAMPLE_THREADS, 1)
+sample_kernel(ResArgs a, int32_t* slots, uint32_t B) {
+  pdl_enter();
+  sample_reservoir(a, slots, B);
+}
+
+// reservoir_sample_batch's commit point and draw in one launch (Reservoir policy): the
+// commit control, then -- after a block barrier, which orders the commit's global writes
+// (p, u, bitmap, seen counters) before the draws -- the sample.  The commit's data plane
+// (commit_copy) follows in the stream; the draws read only slot metadata, never payloads.
+static_assert(CTRL_THREADS == SAMPLE_THREADS, "one block size for both halves");
+__global__ void __launch_bounds__(CTRL_THREADS, 1)
+commit_sample_kernel(ResArgs a, uint64_t tail, uint32_t closed, int32_t* slots, uint32_t B) {
+  pdl_enter();
+  commit_reservoir(a, tail, closed);
+  __syncthreads();
+  sample_reservoir(a, slots, B);
+}
+
 __global__ void gather_inputs(ResArgs a, const int32_t* slots, uint32_t B, uint32_t tau, float* xn) {
   pdl_enter();
   const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -394,6 +427,22 @@ void launch_commit(const ResArgs& a, uint64_t tail, uint32_t closed, uint32_t ma
   dim3 grid(gx);
   if (a.storage == 0) launch_pdl(commit_copy<0>, dim3(grid), dim3(256), 0, s, a);
   else launch_pdl(commit_copy<1>, dim3(grid), dim3(256), 0, s, a);
+}
+
+void launch_commit_sample(const ResArgs& a, uint64_t tail, uint32_t closed, uint32_t max_entries, int32_t* slots,
+                          uint32_t B, cudaStream_t s) {
+  const uint32_t W = (a.C + 31) / 32;
+  const size_t smem = (size_t)(2 * W + 1) * 4;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(commit_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  launch_pdl(commit_sample_kernel, dim3(1), dim3(CTRL_THREADS), smem, s, a, tail, closed, slots, B);
+  if (max_entries == 0) return;
+  const uint32_t n4 = (a.N + 3) / 4;
+  uint32_t gx = (n4 + 255) / 256;
+  const uint32_t cap = 148u * 4u * (max_entries < 4 ? max_entries : 4u);
+  if (gx > cap) gx = cap;
+  if (a.storage == 0) launch_pdl(commit_copy<0>, dim3(gx), dim3(256), 0, s, a);
+  else launch_pdl(commit_copy<1>, dim3(gx), dim3(256), 0, s, a);
 }
 
 void launch_sample(const ResArgs& a, int32_t* slots, uint32_t B, cudaStream_t s) {

@@ -1,6 +1,6 @@
 """A simulation client process for the ingest tests and tools/ingest_bench.py:
 init_communication, send of t in [t0, t1) (fp64 payloads from mel_inputs.clients),
-optionally finalize_communication (P:189)."""
+optionally finalize_communication (P:187)."""
 import argparse
 import os
 import sys

@@ -83,6 +83,11 @@ def test_many_clients_ingest_arrival_order_bit_exact():
     order = list(zip(d["sim"][:total].tolist(), d["t"][:total].tolist()))
     assert sorted(order) == sorted(oi.server_accept(oi.rank_streams([(c, t) for c in range(nc)
                                                                       for t in range(tau)], 1)[0]))
+    # independent of the slot dump's own order: every client sends t = 0, 1, ... in sequence
+    # and takes its ring tickets in that order, so the ring must hand each client's messages
+    # over in send order (a permutation inside the ring breaks this)
+    for c in range(nc):
+        assert [t for (s, t) in order if s == c] == list(range(tau)), c
     res = ores.Reservoir(C, 10, n, seed=5)
     i = 0
     for k in ks:                                      # the same puts between the same commit points
