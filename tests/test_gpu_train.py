@@ -117,6 +117,45 @@ def test_fused_adam_bit_identical_to_unfused(mel, hidden, batch, overlap, monkey
             assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), name
 
 
+@pytest.mark.parametrize("batch,flags", [(256, 0), (128, 8)], ids=["fused-adam", "unfused-adam"])
+def test_k1_result_independent_of_grid(mel, batch, flags, monkeypatch):
+    """Race canary for K1's barrier protocols (compute-sanitizer is not
+    available on this pool): each 128-row tile's forward, gradient and fused Adam depend only
+    on the tile, so the persistent grid's size must not change a single bit of p, m, v.  A
+    grid of 148, 29, 7 or 1 CTA(s) walks every mbarrier ring (H chunks, targets, Y/dY TMEM
+    buffers, Adam stages, early W) through a different phase pattern per CTA (2..79 tiles
+    each); a missed wait or a wrong parity shows up as a difference (or a trap), 25 steps."""
+    wl = _bf16_wl(n=101, batch=batch, capacity=600, threshold=100, sims=40, puts_per_step=40)
+    table = FieldTable(wl)
+    states = []
+    for ctas in (0, 29, 7, 1):
+        if ctas:
+            monkeypatch.setenv("MEL_K1_CTAS", str(ctas))
+        else:
+            monkeypatch.delenv("MEL_K1_CTAS", raising=False)
+        ctx = mel.Context(make_config(wl, precision=1, storage=1, flags=flags))
+        steps = 0
+        for op in design.build_oplog(wl):
+            if op[0] == "PUT":
+                _, r, s, t = op
+                ctx.put(s, t, table.Xs(s), table.field(s, t))
+            elif op[0] == "CLOSE":
+                ctx.close()
+            elif op[0] == "SAMPLE":
+                ctx.sample()
+            elif op[0] == "STEP":
+                if ctx.step()[0] == 0:
+                    steps += 1
+                    if steps == 25:
+                        break
+        assert steps == 25
+        states.append(ctx.get_state())
+    for st in states[1:]:
+        for name in ("p", "m", "v"):
+            for x, y in zip(states[0][name], st[name]):
+                assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), name
+
+
 @pytest.mark.parametrize("precision", [0, 1])
 def test_eval_matches_oracle(mel, precision):
     wl = _bf16_wl(n=40, batch=128)
