@@ -117,9 +117,10 @@ def test_fused_adam_bit_identical_to_unfused(mel, hidden, batch, overlap, monkey
             assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), name
 
 
-@pytest.mark.parametrize("batch,flags", [(256, 0), (320, 0), (128, 8)], ids=["fused-adam", "fused-adam-5-chunks",
-                                                                             "unfused-adam"])
-def test_k1_result_independent_of_grid(mel, batch, flags, monkeypatch):
+@pytest.mark.parametrize("batch,flags,hidden", [(256, 0, (256, 256)), (320, 0, (256, 256)), (128, 8, (256, 256)),
+                                               (448, 0, (128, 128)), (300, 0, (128, 64))],
+                         ids=["fused-adam", "fused-adam-5-chunks", "unfused-adam", "K128-7-chunks", "K64-B300-padded"])
+def test_k1_result_independent_of_grid(mel, batch, flags, hidden, monkeypatch):
     """Race canary for K1's barrier protocols (compute-sanitizer is not
     available on this pool): each 128-row tile's forward, gradient and fused Adam depend only
     on the tile, so the persistent grid's size must not change a single bit of p, m, v.  A
@@ -129,7 +130,7 @@ def test_k1_result_independent_of_grid(mel, batch, flags, monkeypatch):
     B = 320 runs 5 chunks per tile, so the target ring's phase shifts from tile to tile: the
     next tile's targets must not land in the slots the fused Adam still stages in (a bug
     until round 2's end, invisible at <= 1 tile per CTA)."""
-    wl = _bf16_wl(n=101, batch=batch, capacity=600, threshold=100, sims=40, puts_per_step=40)
+    wl = _bf16_wl(n=101, batch=batch, hidden=hidden, capacity=600, threshold=100, sims=40, puts_per_step=40)
     table = FieldTable(wl)
     states = []
     for ctas in (0, 29, 7, 1):
