@@ -117,10 +117,12 @@ def test_fused_adam_bit_identical_to_unfused(mel, hidden, batch, overlap, monkey
             assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), name
 
 
-@pytest.mark.parametrize("batch,flags,hidden", [(256, 0, (256, 256)), (320, 0, (256, 256)), (128, 8, (256, 256)),
-                                               (448, 0, (128, 128)), (300, 0, (128, 64))],
-                         ids=["fused-adam", "fused-adam-5-chunks", "unfused-adam", "K128-7-chunks", "K64-B300-padded"])
-def test_k1_result_independent_of_grid(mel, batch, flags, hidden, monkeypatch):
+@pytest.mark.parametrize("batch,flags,hidden,overlap", [(256, 0, (256, 256), 0), (320, 0, (256, 256), 0),
+                                                       (128, 8, (256, 256), 0), (448, 0, (128, 128), 0),
+                                                       (300, 0, (128, 64), 0), (320, 0, (256, 256), 1)],
+                         ids=["fused-adam", "fused-adam-5-chunks", "unfused-adam", "K128-7-chunks", "K64-B300-padded",
+                              "overlapped-5-chunks"])
+def test_k1_result_independent_of_grid(mel, batch, flags, hidden, overlap, monkeypatch):
     """Race canary for K1's barrier protocols (compute-sanitizer is not
     available on this pool): each 128-row tile's forward, gradient and fused Adam depend only
     on the tile, so the persistent grid's size must not change a single bit of p, m, v.  A
@@ -133,7 +135,10 @@ def test_k1_result_independent_of_grid(mel, batch, flags, hidden, monkeypatch):
     wl = _bf16_wl(n=101, batch=batch, hidden=hidden, capacity=600, threshold=100, sims=40, puts_per_step=40)
     table = FieldTable(wl)
     states = []
-    for ctas in (0, 29, 7, 1):
+    # overlapped variant (opt-in): MMA CTAs hand dW tiles to Adam CTAs through two ring slots
+    # each -- at 7 CTAs (5 MMA + 2 Adam) every MMA CTA recycles its slots many times
+    monkeypatch.setenv("MEL_K1_OVERLAP", str(overlap))
+    for ctas in (0, 29, 7, 2) if overlap else (0, 29, 7, 1):
         if ctas:
             monkeypatch.setenv("MEL_K1_CTAS", str(ctas))
         else:
