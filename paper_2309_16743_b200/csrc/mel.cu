@@ -1033,12 +1033,14 @@ static int create_impl(mel_ctx* c, const mel_config* g, const void* nccl_id, voi
   if (r) return r;
   CK(cudaStreamSynchronize(c->stream));
 
-  // the Adam of W_L inside K1 pays off from 4 batch chunks per tile on (DESIGN.md section 7,
-  // measured step at B = 64 / 128 / 192 / 256: unfused 1.88 / 1.95 / 2.06 / 2.09 ms, fused
-  // 2.77 / 2.80 / 3.64 / 1.79 ms): with fewer chunks the staged Adam phase cannot hide behind
-  // the next tile's MMAs, so small batches (the paper's b = 10) run the separate kernel
+  // the Adam of W_L runs inside K1 at every batch size (end of round 2,
+  // step ms at B = 10 / 64 / 128 / 192 / 256: separate kernel 1.80 / 1.79 / 1.84 / 1.93 / 2.06,
+  // fused 1.57 / 1.59 / 1.65 / 1.73 / 1.77 -- the fused path saves the 2 GB gradient round
+  // trip; early in round 2 it lost below 4 chunks per tile and the policy was B >= 256)
+  uint32_t fused_min_b = 1;
+  if (const char* e = getenv("MEL_FUSED_MIN_B")) fused_min_b = (uint32_t)atoi(e);   // diagnostics (A/B of the policy)
   c->fused_adam = (c->world == 1) && (g->precision == MEL_BF16) && !(g->flags & MEL_FLAG_UNFUSED_ADAM) &&
-                  c->B >= 256;
+                  c->B >= fused_min_b;
   if (c->world > 1) {
     if (!c->virt) {
       ncclUniqueId id;

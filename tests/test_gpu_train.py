@@ -80,8 +80,10 @@ def test_bf16_loss_after_1000_steps_free_running(mel):
 
 
 @pytest.mark.parametrize("hidden,batch,overlap", [((256, 256), 256, False), ((64, 64), 320, False),
-                                                  ((256, 256), 256, True), ((64, 64), 320, True)],
-                         ids=["K256-B256", "K64-B320-padded", "K256-B256-overlapped", "K64-B320-overlapped"])
+                                                  ((256, 256), 256, True), ((64, 64), 320, True),
+                                                  ((256, 256), 10, False), ((256, 256), 64, False)],
+                         ids=["K256-B256", "K64-B320-padded", "K256-B256-overlapped", "K64-B320-overlapped",
+                              "K256-B10-paper", "K256-B64"])
 def test_fused_adam_bit_identical_to_unfused(mel, hidden, batch, overlap, monkeypatch):
     """Adam of W_L inside the output-layer kernel (default at world 1, bf16, B >= 256)
     reproduces the separate Adam kernel bit for bit (master, moments, shadow) over 40
@@ -119,9 +121,10 @@ def test_fused_adam_bit_identical_to_unfused(mel, hidden, batch, overlap, monkey
 
 @pytest.mark.parametrize("batch,flags,hidden,overlap", [(256, 0, (256, 256), 0), (320, 0, (256, 256), 0),
                                                        (128, 8, (256, 256), 0), (448, 0, (128, 128), 0),
-                                                       (300, 0, (128, 64), 0), (320, 0, (256, 256), 1)],
+                                                       (300, 0, (128, 64), 0), (320, 0, (256, 256), 1),
+                                                       (10, 0, (256, 256), 0)],
                          ids=["fused-adam", "fused-adam-5-chunks", "unfused-adam", "K128-7-chunks", "K64-B300-padded",
-                              "overlapped-5-chunks"])
+                              "overlapped-5-chunks", "fused-B10-1-chunk"])
 def test_k1_result_independent_of_grid(mel, batch, flags, hidden, overlap, monkeypatch):
     """Race canary for K1's barrier protocols (compute-sanitizer is not
     available on this pool): each 128-row tile's forward, gradient and fused Adam depend only
