@@ -1209,7 +1209,11 @@ int mel_create_virtual(const mel_config* g, int world, int cuda_device, void* st
     // addressed directly (one device), K1 grid = #SMs / world CTAs per rank
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
-    const int G = sms / world;
+    int G = sms / world;
+    if (const char* e = getenv("MEL_VIRT_CTAS")) {       // diagnostics: fewer K1 CTAs per virtual rank
+      const int v = atoi(e);
+      if (v >= 1 && v < G) G = v;
+    }
     if (cudaMalloc(&vg->d_desc, (size_t)tc::virt_desc_bytes() * world) != cudaSuccess) { cleanup(); return MEL_ENOMEM; }
     for (int q = 0; q < world; ++q) {
       mel_ctx* m = out[q];

@@ -177,3 +177,52 @@ def test_virtual_bf16_1000_steps_free_running(world, mode):
     print("R=%d %s: step-1000 loss rel err %.3e (mean over 951-1000: %.3e); loss %.4e -> %.4e" %
           (world, mode, err, tail, lo_all[0], lo_all[-1]))
     assert err <= 2e-2
+
+
+@pytest.mark.parametrize("world,mode", [(2, "bf16-fp32x")])
+def test_virtual_exchange_independent_of_grid(world, mode, monkeypatch):
+    """Race canary for the in-kernel exchange (TMA store into the owner's acc, acquire/release
+    tile counters, owner-side fused Adam, shadow push to every rank): with G = 74, 16 and 3 K1
+    CTAs per rank every CTA runs 1, ~5 or ~27 tile groups, so the counters, the shadow double
+    buffer and every mbarrier ring go through different phase patterns; the parameters must
+    come out bit-identical after 8 steps (and equal across replicas).  Only R = 2 with fp32
+    contributions is bitwise comparable across grids: the tile -> owner map depends on G
+    (tc::tile_owner), and with bf16 contributions the owner's own dW stays fp32 while the
+    peer's is rounded, so another owner rounds the other term (measured: three grids, three
+    bit patterns, all within the parity bars); at R > 2 the peers' reduce-adds land in
+    arrival order.  fp32 + fp32 in either order is the same sum."""
+    if not _gpu():
+        pytest.skip("needs a GPU")
+    from paper_2309_16743_b200 import mel
+    wl = replace(design.MEDIUM, name="medium-bf16-vr", capacity=600, threshold=100, sims=30, world=world,
+                 batch=128, puts_per_step=60)
+    flags = mel.FLAG_FP32_EXCHANGE if mode.endswith("-fp32x") else 0
+    table = FieldTable(wl)
+    digests = []
+    for g in (0, 16, 3):
+        if g:
+            monkeypatch.setenv("MEL_VIRT_CTAS", str(g))
+        else:
+            monkeypatch.delenv("MEL_VIRT_CTAS", raising=False)
+        vg = mel.VirtualGroup(make_config(wl, precision=1, storage=1, flags=flags), world, device=0)
+        steps = 0
+        for op in design.build_oplog(wl):
+            if op[0] == "PUT":
+                _, r, s, t = op
+                vg.ctx[r].put(s, t, table.Xs(s), table.field(s, t))
+            elif op[0] == "CLOSE":
+                vg.ctx[op[1]].close()
+            elif op[0] == "SAMPLE":
+                vg.ctx[op[1]].sample()
+            elif op[0] == "STEP":
+                if vg.step()[0] == 0:
+                    steps += 1
+                    if steps == 8:
+                        break
+        assert steps == 8
+        states = [vg.ctx[r].get_state() for r in range(world)]
+        hp = {hashlib.sha256(b"".join(x.tobytes() for x in st["p"])).hexdigest() for st in states}
+        assert len(hp) == 1, "replicas diverged at G=%d" % g
+        digests.append(hashlib.sha256(b"".join(x.tobytes() for k in ("p", "m", "v") for x in states[0][k])).hexdigest())
+        vg.close()
+    assert len(set(digests)) == 1, digests
