@@ -18,6 +18,8 @@
 // commit machinery: commit appends while p < C (FIFO at ring slot head + p, FIRO at
 // list position p -> slot pos[p]); FIFO sampling takes the B oldest items, FIRO makes
 // B DRAIN-stream draws with removal (swap with the last list position, in SMEM).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -309,7 +311,8 @@ firo_sample_kernel(ResArgs a, int32_t* slots, uint32_t B) {
   if (threadIdx.x == 0) finish_queue_batch(a, p, n, d + n);
 }
 
-__device__ __forceinline__ void sample_reservoir(const ResArgs& a, int32_t* slots, uint32_t B) {
+// pos_smem: entries of pos[] the caller's dynamic shared memory holds (0: none)
+__device__ __forceinline__ void sample_reservoir(const ResArgs& a, int32_t* slots, uint32_t B, uint32_t pos_smem) {
   __shared__ uint32_t s_cnt;
   ResDev* st = a.st;
   if (threadIdx.x == 0) s_cnt = 0;
@@ -339,32 +342,54 @@ __device__ __forceinline__ void sample_reservoir(const ResArgs& a, int32_t* slot
     }
     return;
   }
-  // drain (P:249-258 with is_reception_over): sequential, each draw removes its item
+  // drain (P:249-258 with is_reception_over): n = min(B, p) draws, each removing its item.
+  // Draw b is k_b = bounded(Philox(DRAIN, d + b), p - b) -- it depends only on b -- so the
+  // draws run in parallel; the removal chain pos[k_b] <- pos[p - 1 - b] runs on one thread,
+  // over pos[] staged in shared memory when it fits; the seen / histogram / u updates touch
+  // distinct slots (no replacement) and run in parallel again.  Same result as drawing one
+  // by one (the round-1 kernel did, on one thread, ~0.1 ms per 1024-draw batch).
+  const uint32_t n = p < B ? p : B;
+  for (uint32_t b = threadIdx.x; b < n; b += blockDim.x)
+    slots[b] = (int32_t)bounded(philox_r64(a.seed, TAG_DRAIN, d + b, a.rank), p - b);
+  extern __shared__ uint32_t s_dyn[];
+  const bool in_smem = p <= pos_smem;
+  uint32_t* pos = in_smem ? s_dyn : a.pos;
+  if (in_smem)
+    for (uint32_t i = threadIdx.x; i < p; i += blockDim.x) s_dyn[i] = a.pos[i];
+  __syncthreads();
   if (threadIdx.x == 0) {
-    uint32_t pp = p, n = 0, u = st->u;
-    uint64_t dd = d;
-    while (n < B && pp > 0) {
-      const uint32_t k = bounded(philox_r64(a.seed, TAG_DRAIN, dd, a.rank), pp);
-      ++dd;
-      const uint32_t j = a.pos[k];
-      const uint32_t sc = a.seen[j];
-      if (sc == 0) --u;
-      a.seen[j] = sc + 1;
-      st->hist[sc + 1 < HIST_BINS ? sc + 1 : HIST_BINS - 1] += 1;
-      slots[n++] = (int32_t)j;
-      a.pos[k] = a.pos[pp - 1];
-      --pp;
+    for (uint32_t b = 0; b < n; ++b) {
+      const uint32_t k = (uint32_t)slots[b];
+      const uint32_t j = pos[k];
+      pos[k] = pos[p - 1 - b];
+      slots[b] = (int32_t)j;
     }
-    st->p = pp; st->u = u; st->d = dd; st->n_last = n;
+  }
+  __syncthreads();
+  if (in_smem)
+    for (uint32_t i = threadIdx.x; i < p; i += blockDim.x) a.pos[i] = s_dyn[i];
+  uint32_t zeros = 0;
+  for (uint32_t b = threadIdx.x; b < n; b += blockDim.x) {
+    const uint32_t j = (uint32_t)slots[b];
+    const uint32_t sc = a.seen[j];
+    a.seen[j] = sc + 1;
+    if (sc == 0) ++zeros;
+    atomicAdd(reinterpret_cast<unsigned long long*>(&st->hist[sc + 1 < HIST_BINS ? sc + 1 : HIST_BINS - 1]), 1ull);
+  }
+  if (zeros) atomicAdd(&s_cnt, zeros);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t u = st->u - s_cnt;
+    st->p = p - n; st->u = u; st->d = d + n; st->n_last = n;
     Mirror* m = a.mirror;
-    m->p = pp; m->u = u; m->d = dd; m->n_last = n; m->over = 1;
+    m->p = p - n; m->u = u; m->d = d + n; m->n_last = n; m->over = 1;
   }
 }
 
 __global__ void __launch_bounds__(SAMPLE_THREADS, 1)
 sample_kernel(ResArgs a, int32_t* slots, uint32_t B) {
   pdl_enter();
-  sample_reservoir(a, slots, B);
+  sample_reservoir(a, slots, B, 0u);
 }
 
 // reservoir_sample_batch's commit point and draw in one launch (Reservoir policy): the
@@ -373,11 +398,11 @@ sample_kernel(ResArgs a, int32_t* slots, uint32_t B) {
 // (commit_copy) follows in the stream; the draws read only slot metadata, never payloads.
 static_assert(CTRL_THREADS == SAMPLE_THREADS, "one block size for both halves");
 __global__ void __launch_bounds__(CTRL_THREADS, 1)
-commit_sample_kernel(ResArgs a, uint64_t tail, uint32_t closed, int32_t* slots, uint32_t B) {
+commit_sample_kernel(ResArgs a, uint64_t tail, uint32_t closed, int32_t* slots, uint32_t B, uint32_t pos_smem) {
   pdl_enter();
   commit_reservoir(a, tail, closed);
-  __syncthreads();
-  sample_reservoir(a, slots, B);
+  __syncthreads();                                  // (the commit is done with the shared memory)
+  sample_reservoir(a, slots, B, pos_smem);
 }
 
 __global__ void gather_inputs(ResArgs a, const int32_t* slots, uint32_t B, uint32_t tau, float* xn) {
@@ -431,11 +456,14 @@ void launch_commit(const ResArgs& a, uint64_t tail, uint32_t closed, uint32_t ma
 
 void launch_commit_sample(const ResArgs& a, uint64_t tail, uint32_t closed, uint32_t max_entries, int32_t* slots,
                           uint32_t B, cudaStream_t s) {
+  // dynamic shared memory: the commit's bitmap + prefix, then (drain) the position list
   const uint32_t W = (a.C + 31) / 32;
-  const size_t smem = (size_t)(2 * W + 1) * 4;
+  constexpr uint32_t POS_SMEM_MAX = 50 * 1024;       // entries (200 KB); larger C drains from global
+  const uint32_t pos_smem = a.C <= POS_SMEM_MAX ? a.C : 0u;
+  const size_t smem = std::max((size_t)(2 * W + 1) * 4, (size_t)pos_smem * 4);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(commit_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  launch_pdl(commit_sample_kernel, dim3(1), dim3(CTRL_THREADS), smem, s, a, tail, closed, slots, B);
+  launch_pdl(commit_sample_kernel, dim3(1), dim3(CTRL_THREADS), smem, s, a, tail, closed, slots, B, pos_smem);
   if (max_entries == 0) return;
   const uint32_t n4 = (a.N + 3) / 4;
   uint32_t gx = (n4 + 255) / 256;
