@@ -213,7 +213,7 @@ commit_copy(ResArgs a) {
   // caller's own field: no staging copy), normalised on the fly
   const uint32_t n_plan = a.st->n_plan;
   const uint32_t n4 = (a.N + 3) / 4;
-  for (uint32_t y = 0; y < n_plan; ++y) {
+  for (uint32_t y = blockIdx.y; y < n_plan; y += gridDim.y) {     // gridDim.y entries at a time
     const uint2 ej = a.plan[y];
     const float* zc = a.plan_src[y];              // zero-copy device put: read the caller's field
     const float4* src = reinterpret_cast<const float4*>(zc ? zc : a.st_field + (uint64_t)ej.x * a.Npad);
@@ -447,9 +447,13 @@ void launch_commit(const ResArgs& a, uint64_t tail, uint32_t closed, uint32_t ma
   if (max_entries == 0) return;
   const uint32_t n4 = (a.N + 3) / 4;
   uint32_t gx = (n4 + 255) / 256;
+#ifndef MEL_CC_ENTRIES
+#define MEL_CC_ENTRIES 4   // entries whose copies run side by side (blockIdx.y)
+#endif
+  const uint32_t gy = max_entries < MEL_CC_ENTRIES ? max_entries : MEL_CC_ENTRIES;   // entries in flight
   const uint32_t cap = 148u * 4u * (max_entries < 4 ? max_entries : 4u);   // ~ one wave per 4 entries
   if (gx > cap) gx = cap;
-  dim3 grid(gx);
+  dim3 grid(gx, gy);
   if (a.storage == 0) launch_pdl(commit_copy<0>, dim3(grid), dim3(256), 0, s, a);
   else launch_pdl(commit_copy<1>, dim3(grid), dim3(256), 0, s, a);
 }
@@ -469,8 +473,9 @@ void launch_commit_sample(const ResArgs& a, uint64_t tail, uint32_t closed, uint
   uint32_t gx = (n4 + 255) / 256;
   const uint32_t cap = 148u * 4u * (max_entries < 4 ? max_entries : 4u);
   if (gx > cap) gx = cap;
-  if (a.storage == 0) launch_pdl(commit_copy<0>, dim3(gx), dim3(256), 0, s, a);
-  else launch_pdl(commit_copy<1>, dim3(gx), dim3(256), 0, s, a);
+  const uint32_t gy = max_entries < MEL_CC_ENTRIES ? max_entries : MEL_CC_ENTRIES;
+  if (a.storage == 0) launch_pdl(commit_copy<0>, dim3(gx, gy), dim3(256), 0, s, a);
+  else launch_pdl(commit_copy<1>, dim3(gx, gy), dim3(256), 0, s, a);
 }
 
 void launch_sample(const ResArgs& a, int32_t* slots, uint32_t B, cudaStream_t s) {
